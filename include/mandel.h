@@ -1,0 +1,217 @@
+/*
+ * mandel.h -- C ABI of the B200-native escape-time Mandelbrot library
+ * (paper_2007_00745_b200/libmandel.so), the boundary of the hot path of
+ * arXiv 2007.00745, "Efficient Generation of Mandelbrot Set using Message
+ * Passing Interface" (Gamage & Baskaran).
+ *
+ * Every step of the path (pixel -> c mapping, escape iteration, store, the
+ * FCFS chunk claims and the gather to rank 0) runs in this library's sm_100a
+ * kernels.  There is no CPU fallback: without a usable CUDA device every
+ * compute entry point returns MANDEL_ENODEV.
+ *
+ * Operation (Eq. 1 and Eq. 2; PAPER.md:179 Cx/Cy arrays):
+ *   dx = (xmax - xmin) / W,   dy = (ymax - ymin) / H,   R2 = R * R   (host, one IEEE op each)
+ *   c(i, j) = (xmin + j*dx, ymax - i*dy)          row 0 is ymax (top-left-corner sampling)
+ *   z0 = 0;  z_{n+1} = z_n^2 + c;  count(i, j) = first n >= 1 with |z_n|^2 > R2, else iterMax
+ *   out[i*W + j] = count(i, j),  1 <= count <= iterMax
+ * Every floating-point operation is a single round-to-nearest-even operation
+ * in the working type, in the order  y' = (x + x)*y + ci;  x' = (x2 - y2) + cr;
+ * x2 = x'*x';  y2 = y'*y';  escape iff x2 + y2 > R2  -- no FMA contraction.
+ * The result is therefore one exact uint32 map per argument set, identical for
+ * every scheme, GPU count and chunk size (Bernstein conditions).
+ *
+ * dtype MANDEL_FP32 computes everything in float: the bounds and R are first
+ * rounded to float, then dx, dy, R2 and the mapping are float operations
+ * (reading R9).
+ *
+ * Partition schemes (§III, 150-225) distribute rows over ngpus GPUs:
+ *   MANDEL_BLOCK   "Naive" rows, Eq. 14-17: rank r owns [q*r, q*(r+1)-1],
+ *                  q = floor(H/N); the last rank also owns the H mod N tail.
+ *   MANDEL_CYCLIC  "Alternating" rows: rank r owns rows
+ *                  r, r+N, ... below floor(H/N)*N; rank 0 owns the tail.
+ *   MANDEL_FCFS    "First Come First Served": GPUs claim
+ *                  chunk_rows-row chunks from one atomic counter in GPU 0's
+ *                  memory (system-scope atomics over NVLink); no master GPU.
+ * Each GPU's kernel stores its counts directly into GPU 0's image (peer
+ * stores over NVLink): the paper's "send to master" without a
+ * separate gather or the alternating scheme's reconstruction pass.
+ *
+ * Threading: calls are serialised inside the library; a call that finds
+ * another in progress returns MANDEL_EBUSY.  All calls are synchronous: they
+ * return when the map is complete in the requested destination.
+ */
+#ifndef MANDEL_H
+#define MANDEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MANDEL_ABI_VERSION 1
+#define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
+#define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
+
+enum mandel_dtype { MANDEL_FP64 = 0, MANDEL_FP32 = 1 };
+
+enum mandel_scheme {
+    MANDEL_BLOCK = 0,   /* paper "Naive" row segmentation, Eq. 14-17     */
+    MANDEL_CYCLIC = 1,  /* paper "Alternating" row segmentation          */
+    MANDEL_FCFS = 2     /* paper "First Come First Served" (chunked)     */
+};
+
+enum mandel_status {
+    MANDEL_OK = 0,
+    MANDEL_EINVAL = -1,  /* an argument is out of its documented domain                */
+    MANDEL_ENODEV = -2,  /* no CUDA device, too few devices, or no peer access         */
+    MANDEL_ENOMEM = -3,  /* device or pinned allocation failed                         */
+    MANDEL_ECUDA = -4,   /* a CUDA runtime call failed (detail: mandel_last_error)      */
+    MANDEL_ECOMM = -5,   /* inter-GPU / inter-process plumbing failed (IPC, peer map)   */
+    MANDEL_EBUSY = -6    /* another call is in progress                                */
+};
+
+enum mandel_kernel {
+    MANDEL_KERNEL_REFILL = 0,  /* persistent CTAs, per-warp tile queue, lane refill (default) */
+    MANDEL_KERNEL_STATIC = 1   /* one pixel per thread, static grid (baseline; BLOCK/CYCLIC only) */
+};
+
+/* Per-call statistics (all fields written when stats != NULL and the call succeeds). */
+typedef struct mandel_stats {
+    double   device_ms;            /* synchronised start on all GPUs -> GPU 0 holds the full map     */
+    double   kernel_ms_max;        /* max over ranks of the escape kernel's CUDA-event time          */
+    double   kernel_ms[MANDEL_MAX_GPUS];
+    double   d2h_ms;               /* device -> host copy of the map (0 if out_host == NULL)         */
+    double   total_ms;             /* host wall time of the whole call                               */
+    uint64_t sum_iters;            /* sum of all counts = pixel-iterations performed                 */
+    uint64_t pixels;               /* pixels written (W*H when complete)                             */
+    uint64_t rank_iters[MANDEL_MAX_GPUS];  /* per-rank pixel-iterations                            */
+    uint64_t rank_pixels[MANDEL_MAX_GPUS]; /* per-rank pixels                                      */
+    uint32_t rank_rows[MANDEL_MAX_GPUS];   /* per-rank rows started (FCFS: claimed chunk rows)     */
+    uint32_t chunks_claimed;       /* FCFS successful global claims (= ceil(H/chunk_rows)); Eq. 19  */
+    uint32_t transfers;            /* rank->rank-0 result streams: N-1 (Eq. 18/20), FCFS: claims by
+                                      ranks != 0                                                     */
+    uint32_t kernel_launches;      /* kernels this call launched                                    */
+    uint32_t ngpus;                /* ranks used                                                    */
+    uint32_t ndevices;             /* distinct physical devices used                                */
+} mandel_stats;
+
+/* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
+typedef struct mandel_options {
+    uint32_t chunk_rows;     /* FCFS rows per claim; 0 -> 16 (BASELINE.json C5)                   */
+    uint32_t tile_px;        /* pixels per warp tile (refill kernel); 0 -> library default        */
+    int      kernel;         /* enum mandel_kernel                                                */
+    int      logical_ranks;  /* nonzero: allow ngpus > device count, rank g runs on device
+                                g % count on its own stream (tests; ranks never wait on each other) */
+    int      reserved[4];
+} mandel_options;
+
+/*
+ * mandel_render -- BASELINE.json north_star entry point.
+ *   xmin < xmax, ymin < ymax : the complex window (finite doubles)
+ *   W, H      : image width (columns, real axis) and height (rows, imaginary axis), >= 1
+ *   iterMax   : iteration cap ("iterationMax"), >= 1
+ *   R         : escape RADIUS (> 0, R*R finite in dtype); escape is |z|^2 > R*R.
+ *               The paper's "Escape Radius 400" is R = 20 (R1).
+ *   dtype     : enum mandel_dtype
+ *   scheme    : enum mandel_scheme
+ *   ngpus     : GPUs 0..ngpus-1 (1 <= ngpus <= device count)
+ *   out_u32   : HOST buffer of W*H uint32, row-major, caller-owned (pinned recommended)
+ * Returns MANDEL_OK or a negative mandel_status; on error out_u32 is unspecified.
+ * EINVAL: W or H == 0; W*H*4 overflows size_t; iterMax == 0; R <= 0 or non-finite or
+ *   R*R non-finite (in dtype); any bound non-finite (in dtype); xmin >= xmax or
+ *   ymin >= ymax (after rounding, for fp32); dx or dy == 0 in dtype; dtype/scheme out of
+ *   range; out_u32 == NULL; BLOCK/CYCLIC with H < ngpus.
+ * ENODEV: ngpus < 1, ngpus > devices, no CUDA device, or peer access unavailable.
+ */
+int mandel_render(double xmin, double xmax, double ymin, double ymax,
+                  uint32_t W, uint32_t H, uint32_t iterMax, double R,
+                  int dtype, int scheme, int ngpus, uint32_t *out_u32);
+
+/*
+ * mandel_render_ex -- mandel_render with options, statistics and device output.
+ *   out_host : nullable HOST destination (W*H uint32); copied device->host at the end.
+ *   out_dev0 : nullable DEVICE pointer on device 0 (caller-owned, >= W*H*4 bytes,
+ *              4-byte aligned) that receives the map; if NULL the library uses a
+ *              cached buffer it owns.  At least one of out_host / out_dev0 is required.
+ *   stream0  : nullable cudaStream_t on device 0; rank 0's work (and the D2H copy) is
+ *              ordered on it, so a caller can time the call with events on that stream.
+ *   opts     : nullable options;  stats : nullable statistics.
+ * Errors as mandel_render; EINVAL also when both outputs are NULL.
+ */
+int mandel_render_ex(double xmin, double xmax, double ymin, double ymax,
+                     uint32_t W, uint32_t H, uint32_t iterMax, double R,
+                     int dtype, int scheme, int ngpus,
+                     const mandel_options *opts,
+                     uint32_t *out_host, uint32_t *out_dev0, void *stream0,
+                     mandel_stats *stats);
+
+/*
+ * mandel_render_rank -- one rank of a multi-PROCESS render (one process per GPU,
+ * e.g. under torchrun).  The caller's process runs rank `rank` of `nranks` on the
+ * current CUDA device and:
+ *   out_root     : DEVICE pointer, valid in this process, to rank 0's W*H uint32 image
+ *                  (rank 0: its own buffer; others: mapped with mandel_ipc_open).
+ *   fcfs_counter : DEVICE pointer to a uint32 chunk counter shared by all ranks (rank 0's
+ *                  memory, IPC-mapped elsewhere); must be 0 before any rank starts and is
+ *                  only used by MANDEL_FCFS (may be NULL otherwise).  The caller resets it
+ *                  and separates renders with a barrier.
+ *   stream       : nullable cudaStream_t of the current device.
+ * The call returns when this rank's rows are stored in the root image.  stats (nullable)
+ * receives this rank's kernel_ms / rank_iters[0] / rank_pixels[0] / chunks_claimed.
+ * Errors: as mandel_render_ex, plus EINVAL for rank outside [0, nranks) or a NULL out_root,
+ * or FCFS with a NULL fcfs_counter.
+ */
+int mandel_render_rank(double xmin, double xmax, double ymin, double ymax,
+                       uint32_t W, uint32_t H, uint32_t iterMax, double R,
+                       int dtype, int scheme, int rank, int nranks,
+                       const mandel_options *opts,
+                       uint32_t *out_root, uint32_t *fcfs_counter, void *stream,
+                       mandel_stats *stats);
+
+/*
+ * Device memory shared across processes (CUDA IPC).  mandel_dev_alloc returns a
+ * cudaMalloc'd block on `device` (so IPC handles address it at offset 0);
+ * mandel_ipc_handle writes MANDEL_IPC_HANDLE_BYTES bytes describing it;
+ * mandel_ipc_open maps another process's block into this process (on the current
+ * device, peer access enabled lazily); mandel_ipc_close unmaps it.
+ * Errors: EINVAL on NULL arguments, ENOMEM, ECOMM when the IPC call fails.
+ */
+int mandel_dev_alloc(int device, size_t bytes, void **dev_ptr);
+int mandel_dev_free(void *dev_ptr);
+int mandel_ipc_handle(void *dev_ptr, void *handle_out);
+int mandel_ipc_open(const void *handle, void **dev_ptr_out);
+int mandel_ipc_close(void *dev_ptr);
+/* Zero `bytes` bytes at dev_ptr (any device pointer valid in this process) on `stream`
+ * (nullable = the legacy default stream of the current device) and wait for it.
+ * Used to reset the shared FCFS counter between multi-process renders. */
+int mandel_dev_zero(void *dev_ptr, size_t bytes, void *stream);
+
+/*
+ * mandel_plan_rows -- host-only planner of the static schemes (no GPU needed).
+ * Writes the rows rank `rank` of `ngpus` owns under `scheme` (BLOCK: Eq. 14-17;
+ * CYCLIC: PAPER.md:217-218), ascending, to rows_out (nullable: then only *count is
+ * written).  *count must hold the capacity of rows_out on entry when rows_out != NULL.
+ * EINVAL: scheme FCFS (dynamic) or out of range, ngpus < 1, H < ngpus, rank outside
+ * [0, ngpus), count NULL, or capacity too small (then *count = rows needed).
+ */
+int mandel_plan_rows(int scheme, uint32_t H, int ngpus, int rank,
+                     uint32_t *rows_out, uint32_t *count);
+
+/* Static description of a status code (never NULL). */
+const char *mandel_strerror(int code);
+/* Detail string of the calling thread's last failure ("" if none). */
+const char *mandel_last_error(void);
+/* Number of visible CUDA devices (0 when none or the driver is unusable). */
+int mandel_device_count(void);
+/* Frees cached device buffers, streams and events on every device. */
+void mandel_shutdown(void);
+/* MANDEL_ABI_VERSION of the loaded library. */
+int mandel_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MANDEL_H */

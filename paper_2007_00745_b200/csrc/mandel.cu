@@ -1,0 +1,673 @@
+// mandel.cu -- host runtime and C ABI (include/mandel.h) of the B200 escape-time library.
+//
+// Layers: L1 device kernels (mandel_kernels.cuh) <- L2 this host runtime
+// (validation, step a1 constants, partition plans, per-device contexts, launches,
+// statistics) <- L3 the extern "C" functions at the bottom.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
+//        -Xcompiler -fPIC,-ffp-contract=off -shared -Iinclude -o libmandel.so mandel.cu
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mandel.h"
+#include "mandel_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_detail;
+
+int fail(int code, const std::string& what) {
+    g_detail = what;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_detail = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    if (e == cudaErrorMemoryAllocation) return MANDEL_ENOMEM;
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return MANDEL_ENODEV;
+    return MANDEL_ECUDA;
+}
+
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Step a1: validation and derived constants (SURVEY.md §8(a) a1, §8(b) errors).
+// dx = (xmax - xmin)/W, dy = (ymax - ymin)/H, R2 = R*R, each one IEEE operation in
+// the working type; fp32 first rounds the bounds and R to float (R9).
+// ---------------------------------------------------------------------------
+struct Derived {
+    double xmin, ymax, dx, dy;
+    float xminf, ymaxf, dxf, dyf;
+    long long r2bits;
+};
+
+int derive(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
+           uint32_t iter_max, double R, int dtype, Derived& d) {
+    if (W == 0 || H == 0) return fail(MANDEL_EINVAL, "W and H must be >= 1");
+    if ((uint64_t)W * (uint64_t)H > (uint64_t)(SIZE_MAX / 4)) return fail(MANDEL_EINVAL, "W*H*4 overflows size_t");
+    if (iter_max == 0) return fail(MANDEL_EINVAL, "iterMax must be >= 1");
+    if (dtype != MANDEL_FP64 && dtype != MANDEL_FP32) return fail(MANDEL_EINVAL, "dtype out of range");
+    if (!std::isfinite(xmin) || !std::isfinite(xmax) || !std::isfinite(ymin) || !std::isfinite(ymax))
+        return fail(MANDEL_EINVAL, "window bounds must be finite");
+    if (!(xmin < xmax) || !(ymin < ymax)) return fail(MANDEL_EINVAL, "need xmin < xmax and ymin < ymax");
+    if (!std::isfinite(R) || !(R > 0.0)) return fail(MANDEL_EINVAL, "R must be finite and > 0");
+    std::memset(&d, 0, sizeof(d));
+    if (dtype == MANDEL_FP64) {
+        volatile double r2 = R * R;
+        if (!std::isfinite((double)r2) || !(r2 > 0.0)) return fail(MANDEL_EINVAL, "R*R not finite/positive in fp64");
+        volatile double dx = (xmax - xmin) / (double)W;
+        volatile double dy = (ymax - ymin) / (double)H;
+        if (!(dx > 0.0) || !(dy > 0.0) || !std::isfinite((double)dx) || !std::isfinite((double)dy))
+            return fail(MANDEL_EINVAL, "window collapses (dx or dy not positive/finite)");
+        d.xmin = xmin;
+        d.ymax = ymax;
+        d.dx = dx;
+        d.dy = dy;
+        double r2v = r2;
+        std::memcpy(&d.r2bits, &r2v, 8);
+        return MANDEL_OK;
+    }
+    volatile float xa = (float)xmin, xb = (float)xmax, ya = (float)ymin, yb = (float)ymax, Rf = (float)R;
+    if (!std::isfinite((float)xa) || !std::isfinite((float)xb) || !std::isfinite((float)ya) ||
+        !std::isfinite((float)yb) || !std::isfinite((float)Rf))
+        return fail(MANDEL_EINVAL, "bounds or R not finite in fp32");
+    if (!(xa < xb) || !(ya < yb)) return fail(MANDEL_EINVAL, "window collapses after rounding to fp32");
+    if (!(Rf > 0.0f)) return fail(MANDEL_EINVAL, "R rounds to 0 in fp32");
+    volatile float r2 = Rf * Rf;
+    if (!std::isfinite((float)r2) || !(r2 > 0.0f)) return fail(MANDEL_EINVAL, "R*R not finite/positive in fp32");
+    volatile float dx = (xb - xa) / (float)W;
+    volatile float dy = (yb - ya) / (float)H;
+    if (!(dx > 0.0f) || !(dy > 0.0f) || !std::isfinite((float)dx) || !std::isfinite((float)dy))
+        return fail(MANDEL_EINVAL, "window collapses in fp32 (dx or dy == 0)");
+    d.xminf = xa;
+    d.ymaxf = yb;
+    d.dxf = dx;
+    d.dyf = dy;
+    float r2v = r2;
+    int32_t b;
+    std::memcpy(&b, &r2v, 4);
+    d.r2bits = b;
+    return MANDEL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Step a2: static partition plans (§III).  A plan is a slot->row map
+//   row(s) = s < count0 ? base0 + s*stride0 : base1 + (s - count0),  s < nslots.
+// ---------------------------------------------------------------------------
+struct Plan {
+    uint32_t nslots, base0, stride0, count0, base1;
+};
+
+int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
+    if (n < 1) return fail(MANDEL_EINVAL, "ngpus must be >= 1");
+    if (r < 0 || r >= n) return fail(MANDEL_EINVAL, "rank out of range");
+    const uint32_t N = (uint32_t)n, R = (uint32_t)r;
+    if (scheme == MANDEL_BLOCK || scheme == MANDEL_CYCLIC) {
+        if (H < N) return fail(MANDEL_EINVAL, "static schemes need H >= ngpus");
+        const uint32_t q = H / N;  // Eq. 16, rows per task
+        if (scheme == MANDEL_BLOCK) {
+            // Eq. 14: S_r = q*r;  Eq. 15 (read (r+1)): E_r = q*(r+1) - 1;  Eq. 17: last rank += H mod N
+            const uint32_t rows = q + (R == N - 1 ? H % N : 0);
+            pl = Plan{rows, q * R, 1, rows, 0};
+        } else {
+            // Alternating: r, r+N, ... below q*N; the master (rank 0) takes the tail [q*N, H)
+            const uint32_t tail = (R == 0) ? H - q * N : 0;
+            pl = Plan{q + tail, R, N, q, q * N};
+        }
+        return MANDEL_OK;
+    }
+    if (scheme == MANDEL_FCFS) {
+        pl = Plan{0, 0, 0, 0, 0};
+        return MANDEL_OK;
+    }
+    return fail(MANDEL_EINVAL, "scheme out of range");
+}
+
+// ---------------------------------------------------------------------------
+// Per-device and per-rank resources (cached across calls; freed by mandel_shutdown).
+// ---------------------------------------------------------------------------
+struct DeviceCtx {
+    bool init = false;
+    int sms = 0;
+    int occ_refill[2] = {0, 0};  // CTAs/SM, [fp64, fp32]
+    int occ_static[2] = {0, 0};
+    bool peer_to0 = false;
+};
+
+struct RankCtx {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t k0 = nullptr, k1 = nullptr;
+    void* state = nullptr;  // WorkState + chunk_map
+    size_t state_bytes = 0;
+};
+
+struct Root {
+    uint32_t* image = nullptr;  // library-owned map on device 0
+    size_t image_bytes = 0;
+    uint32_t* fcfs_ctr = nullptr;
+    cudaEvent_t start = nullptr, done = nullptr, d2h = nullptr;
+};
+
+std::mutex g_mu;
+std::atomic<bool> g_busy{false};
+std::vector<DeviceCtx> g_dev;
+RankCtx g_rank[MANDEL_MAX_GPUS];
+Root g_root;
+
+struct BusyGuard {
+    bool ok;
+    BusyGuard() { bool f = false; ok = g_busy.compare_exchange_strong(f, true); }
+    ~BusyGuard() { if (ok) g_busy.store(false); }
+};
+
+int device_count(int& n) {
+    n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = 0;
+        return fail(MANDEL_ENODEV, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    if ((int)g_dev.size() < n) g_dev.resize(n);
+    return MANDEL_OK;
+}
+
+int ensure_device(int dev) {
+    DeviceCtx& d = g_dev[dev];
+    if (d.init) return MANDEL_OK;
+    CK(cudaSetDevice(dev));
+    CK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_refill[0], mandel::escape_refill_kernel<double>, mandel::kCtaThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_refill[1], mandel::escape_refill_kernel<float>, mandel::kCtaThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_static[0], mandel::escape_static_kernel<double>, mandel::kCtaThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_static[1], mandel::escape_static_kernel<float>, mandel::kCtaThreads, 0));
+    d.init = true;
+    return MANDEL_OK;
+}
+
+int ensure_peer(int dev) {
+    if (dev == 0) return MANDEL_OK;
+    DeviceCtx& d = g_dev[dev];
+    if (d.peer_to0) return MANDEL_OK;
+    int can = 0;
+    CK(cudaDeviceCanAccessPeer(&can, dev, 0));
+    if (!can) return fail(MANDEL_ENODEV, "peer access from device " + std::to_string(dev) + " to device 0 unavailable");
+    CK(cudaSetDevice(dev));
+    cudaError_t e = cudaDeviceEnablePeerAccess(0, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    d.peer_to0 = true;
+    return MANDEL_OK;
+}
+
+int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
+    RankCtx& rc = g_rank[r];
+    if (rc.device != dev) {
+        if (rc.device >= 0) {
+            cudaSetDevice(rc.device);
+            if (rc.stream) cudaStreamDestroy(rc.stream);
+            if (rc.k0) cudaEventDestroy(rc.k0);
+            if (rc.k1) cudaEventDestroy(rc.k1);
+            if (rc.state) cudaFree(rc.state);
+            rc = RankCtx();
+        }
+        rc.device = dev;
+    }
+    CK(cudaSetDevice(dev));
+    if (!rc.stream) CK(cudaStreamCreateWithFlags(&rc.stream, cudaStreamNonBlocking));
+    if (!rc.k0) CK(cudaEventCreate(&rc.k0));
+    if (!rc.k1) CK(cudaEventCreate(&rc.k1));
+    if (rc.state_bytes < state_bytes) {
+        if (rc.state) CK(cudaFree(rc.state));
+        rc.state = nullptr;
+        rc.state_bytes = 0;
+        CK(cudaMalloc(&rc.state, state_bytes));
+        rc.state_bytes = state_bytes;
+    }
+    (void)user_stream;
+    return MANDEL_OK;
+}
+
+constexpr uint32_t kDefaultTile = 256;
+constexpr uint32_t kDefaultChunk = 16;
+
+struct LaunchSpec {
+    mandel::Params p;
+    dim3 grid, block;
+    bool refill;
+    bool fp32;
+};
+
+int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
+                 int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
+                 uint32_t* fcfs_ctr, int device, LaunchSpec& ls) {
+    Plan pl;
+    int rc = make_plan(scheme, H, nranks, rank, pl);
+    if (rc) return rc;
+    const int kernel = o ? o->kernel : MANDEL_KERNEL_REFILL;
+    if (kernel != MANDEL_KERNEL_REFILL && kernel != MANDEL_KERNEL_STATIC)
+        return fail(MANDEL_EINVAL, "options.kernel out of range");
+    if (kernel == MANDEL_KERNEL_STATIC && scheme == MANDEL_FCFS)
+        return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
+    const uint32_t chunk = (o && o->chunk_rows) ? o->chunk_rows : kDefaultChunk;
+    uint32_t tile = (o && o->tile_px) ? o->tile_px : kDefaultTile;
+    if (tile > W) tile = W;
+    mandel::Params& p = ls.p;
+    std::memset(&p, 0, sizeof(p));
+    p.xmin = d.xmin; p.ymax = d.ymax; p.dx = d.dx; p.dy = d.dy;
+    p.xminf = d.xminf; p.ymaxf = d.ymaxf; p.dxf = d.dxf; p.dyf = d.dyf;
+    p.r2bits = d.r2bits;
+    p.W = W; p.H = H; p.iter_max = iter_max;
+    p.scheme = (uint32_t)scheme;
+    p.tile_w = tile;
+    p.tiles_per_row = (W + tile - 1) / tile;
+    p.nslots = pl.nslots; p.base0 = pl.base0; p.stride0 = pl.stride0; p.count0 = pl.count0; p.base1 = pl.base1;
+    p.chunk_rows = chunk;
+    p.nchunks = (uint32_t)(((uint64_t)H + chunk - 1) / chunk);
+    if (scheme == MANDEL_FCFS) {
+        uint64_t tiles = (uint64_t)(p.nchunks + 1) * chunk * p.tiles_per_row;
+        if (tiles >= 0xF0000000ull) return fail(MANDEL_EINVAL, "FCFS tile space exceeds 32 bits; raise tile_px");
+    } else if ((uint64_t)p.nslots * p.tiles_per_row >= 0xF0000000ull) {
+        return fail(MANDEL_EINVAL, "tile space exceeds 32 bits; raise tile_px");
+    }
+    p.out = out;
+    p.ws = reinterpret_cast<mandel::WorkState*>(state);
+    p.chunk_map = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(state) + sizeof(mandel::WorkState));
+    p.fcfs_ctr = fcfs_ctr;
+    const DeviceCtx& dc = g_dev[device];
+    const int fi = dtype == MANDEL_FP32 ? 1 : 0;
+    ls.fp32 = fi == 1;
+    ls.refill = kernel == MANDEL_KERNEL_REFILL;
+    ls.block = ls.refill ? dim3(mandel::kCtaThreads) : dim3(32, mandel::kWarpsPerCta);
+    if (ls.refill) {
+        int occ = dc.occ_refill[fi] > 0 ? dc.occ_refill[fi] : 1;
+        ls.grid = dim3((unsigned)(occ * dc.sms));
+    } else {
+        ls.grid = dim3((W + 31) / 32, (pl.nslots + mandel::kWarpsPerCta - 1) / mandel::kWarpsPerCta);
+        if (pl.nslots == 0) ls.grid.y = 1;
+    }
+    return MANDEL_OK;
+}
+
+size_t state_bytes_for(uint32_t H, const mandel_options* o) {
+    const uint32_t chunk = (o && o->chunk_rows) ? o->chunk_rows : kDefaultChunk;
+    const uint64_t nchunks = ((uint64_t)H + chunk - 1) / chunk;
+    return sizeof(mandel::WorkState) + (nchunks + 2) * sizeof(uint32_t);
+}
+
+int launch(const LaunchSpec& ls, cudaStream_t s) {
+    if (ls.refill) {
+        if (ls.fp32) mandel::escape_refill_kernel<float><<<ls.grid, ls.block, 0, s>>>(ls.p);
+        else mandel::escape_refill_kernel<double><<<ls.grid, ls.block, 0, s>>>(ls.p);
+    } else {
+        if (ls.fp32) mandel::escape_static_kernel<float><<<ls.grid, ls.block, 0, s>>>(ls.p);
+        else mandel::escape_static_kernel<double><<<ls.grid, ls.block, 0, s>>>(ls.p);
+    }
+    CK(cudaGetLastError());
+    return MANDEL_OK;
+}
+
+double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
+                uint32_t iter_max, double R, int dtype, int scheme, int ngpus,
+                const mandel_options* opts, uint32_t* out_host, uint32_t* out_dev0,
+                void* stream0v, mandel_stats* stats) {
+    const double t_call = now_ms();
+    Derived d;
+    int rc = derive(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, d);
+    if (rc) return rc;
+    if (scheme < MANDEL_BLOCK || scheme > MANDEL_FCFS) return fail(MANDEL_EINVAL, "scheme out of range");
+    if (!out_host && !out_dev0) return fail(MANDEL_EINVAL, "need out_host or out_dev0");
+    if (ngpus < 1 || ngpus > MANDEL_MAX_GPUS) return fail(MANDEL_ENODEV, "ngpus out of range");
+    if (scheme != MANDEL_FCFS && H < (uint32_t)ngpus) return fail(MANDEL_EINVAL, "static schemes need H >= ngpus");
+    if (opts && opts->kernel == MANDEL_KERNEL_STATIC && scheme == MANDEL_FCFS)
+        return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
+    int ndev = 0;
+    rc = device_count(ndev);
+    if (rc) return rc;
+    const bool logical = opts && opts->logical_ranks;
+    if (ngpus > ndev && !logical) return fail(MANDEL_ENODEV, "ngpus exceeds the visible device count");
+    const int nphys = ngpus < ndev ? ngpus : ndev;
+    for (int g = 0; g < nphys; ++g) {
+        rc = ensure_device(g);
+        if (rc) return rc;
+        rc = ensure_peer(g);
+        if (rc) return rc;
+    }
+    const size_t bytes = (size_t)W * H * sizeof(uint32_t);
+    CK(cudaSetDevice(0));
+    if (!g_root.start) {
+        CK(cudaEventCreate(&g_root.start));
+        CK(cudaEventCreate(&g_root.done));
+        CK(cudaEventCreate(&g_root.d2h));
+    }
+    if (!g_root.fcfs_ctr) CK(cudaMalloc(&g_root.fcfs_ctr, 256));
+    uint32_t* image = out_dev0;
+    if (!image) {
+        if (g_root.image_bytes < bytes) {
+            if (g_root.image) CK(cudaFree(g_root.image));
+            g_root.image = nullptr;
+            g_root.image_bytes = 0;
+            CK(cudaMalloc(&g_root.image, bytes));
+            g_root.image_bytes = bytes;
+        }
+        image = g_root.image;
+    }
+    const size_t sbytes = state_bytes_for(H, opts);
+    std::vector<LaunchSpec> specs(ngpus);
+    for (int r = 0; r < ngpus; ++r) {
+        const int dev = r % ndev;
+        rc = ensure_rank(r, dev, sbytes, nullptr);
+        if (rc) return rc;
+        rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, g_rank[r].state,
+                          g_root.fcfs_ctr, dev, specs[r]);
+        if (rc) return rc;
+    }
+    cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
+    // rank 0 orders everything: reset state, start event, then every rank waits on it
+    CK(cudaSetDevice(0));
+    CK(cudaMemsetAsync(g_root.fcfs_ctr, 0, 256, s0));
+    CK(cudaMemsetAsync(g_rank[0].state, 0, sbytes, s0));
+    CK(cudaEventRecord(g_root.start, s0));
+    for (int r = 1; r < ngpus; ++r) {
+        RankCtx& rk = g_rank[r];
+        CK(cudaSetDevice(rk.device));
+        CK(cudaStreamWaitEvent(rk.stream, g_root.start, 0));
+        CK(cudaMemsetAsync(rk.state, 0, sbytes, rk.stream));
+    }
+    int launches = 0;
+    for (int r = 0; r < ngpus; ++r) {
+        RankCtx& rk = g_rank[r];
+        cudaStream_t s = r == 0 ? s0 : rk.stream;
+        CK(cudaSetDevice(rk.device));
+        CK(cudaEventRecord(rk.k0, s));
+        rc = launch(specs[r], s);
+        if (rc) return rc;
+        ++launches;
+        CK(cudaEventRecord(rk.k1, s));
+    }
+    CK(cudaSetDevice(0));
+    for (int r = 1; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].k1, 0));
+    CK(cudaEventRecord(g_root.done, s0));
+    if (out_host) {
+        CK(cudaMemcpyAsync(out_host, image, bytes, cudaMemcpyDeviceToHost, s0));
+        CK(cudaEventRecord(g_root.d2h, s0));
+    }
+    // read back per-rank statistics (small, ordered after each rank's kernel)
+    std::vector<mandel::WorkState> ws(ngpus);
+    for (int r = 0; r < ngpus; ++r) {
+        RankCtx& rk = g_rank[r];
+        CK(cudaSetDevice(rk.device));
+        CK(cudaMemcpyAsync(&ws[r], rk.state, sizeof(mandel::WorkState), cudaMemcpyDeviceToHost,
+                           r == 0 ? s0 : rk.stream));
+    }
+    for (int r = 0; r < ngpus; ++r) {
+        RankCtx& rk = g_rank[r];
+        CK(cudaSetDevice(rk.device));
+        CK(cudaStreamSynchronize(r == 0 ? s0 : rk.stream));
+    }
+    CK(cudaSetDevice(0));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, g_root.start, g_root.done));
+        stats->device_ms = ms;
+        if (out_host) {
+            CK(cudaEventElapsedTime(&ms, g_root.done, g_root.d2h));
+            stats->d2h_ms = ms;
+        }
+        uint32_t claims = 0, transfers = 0;
+        for (int r = 0; r < ngpus; ++r) {
+            CK(cudaEventElapsedTime(&ms, g_rank[r].k0, g_rank[r].k1));
+            stats->kernel_ms[r] = ms;
+            if (ms > stats->kernel_ms_max) stats->kernel_ms_max = ms;
+            stats->rank_iters[r] = ws[r].sum_iters;
+            stats->rank_pixels[r] = ws[r].pixels;
+            stats->rank_rows[r] = ws[r].rows_started;
+            stats->sum_iters += ws[r].sum_iters;
+            stats->pixels += ws[r].pixels;
+            claims += ws[r].chunks_claimed;
+            if (r != 0) transfers += scheme == MANDEL_FCFS ? ws[r].chunks_claimed : 1u;
+        }
+        stats->chunks_claimed = claims;
+        stats->transfers = transfers;
+        stats->kernel_launches = (uint32_t)launches;
+        stats->ngpus = (uint32_t)ngpus;
+        stats->ndevices = (uint32_t)nphys;
+        stats->total_ms = now_ms() - t_call;
+    }
+    return MANDEL_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int mandel_abi_version(void) { return MANDEL_ABI_VERSION; }
+
+const char* mandel_strerror(int code) {
+    switch (code) {
+        case MANDEL_OK: return "ok";
+        case MANDEL_EINVAL: return "invalid argument";
+        case MANDEL_ENODEV: return "no usable CUDA device / peer access";
+        case MANDEL_ENOMEM: return "out of memory";
+        case MANDEL_ECUDA: return "CUDA runtime error";
+        case MANDEL_ECOMM: return "inter-GPU communication error";
+        case MANDEL_EBUSY: return "library busy (concurrent call)";
+        default: return "unknown status";
+    }
+}
+
+const char* mandel_last_error(void) { return g_detail.c_str(); }
+
+int mandel_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int mandel_plan_rows(int scheme, uint32_t H, int ngpus, int rank, uint32_t* rows_out, uint32_t* count) {
+    if (!count) return fail(MANDEL_EINVAL, "count must not be NULL");
+    if (scheme == MANDEL_FCFS) return fail(MANDEL_EINVAL, "FCFS is dynamic: no static plan");
+    if (scheme != MANDEL_BLOCK && scheme != MANDEL_CYCLIC) return fail(MANDEL_EINVAL, "scheme out of range");
+    Plan pl;
+    int rc = make_plan(scheme, H, ngpus, rank, pl);
+    if (rc) return rc;
+    if (rows_out) {
+        if (*count < pl.nslots) {
+            *count = pl.nslots;
+            return fail(MANDEL_EINVAL, "rows_out capacity too small");
+        }
+        for (uint32_t s = 0; s < pl.nslots; ++s)
+            rows_out[s] = s < pl.count0 ? pl.base0 + s * pl.stride0 : pl.base1 + (s - pl.count0);
+    }
+    *count = pl.nslots;
+    return MANDEL_OK;
+}
+
+int mandel_render_ex(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
+                     uint32_t iterMax, double R, int dtype, int scheme, int ngpus,
+                     const mandel_options* opts, uint32_t* out_host, uint32_t* out_dev0,
+                     void* stream0, mandel_stats* stats) {
+    BusyGuard busy;
+    if (!busy.ok) return fail(MANDEL_EBUSY, "another mandel call is in progress");
+    std::lock_guard<std::mutex> lk(g_mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaGetLastError();
+    int rc = render_impl(xmin, xmax, ymin, ymax, W, H, iterMax, R, dtype, scheme, ngpus, opts,
+                         out_host, out_dev0, stream0, stats);
+    cudaSetDevice(prev);
+    cudaGetLastError();
+    return rc;
+}
+
+int mandel_render(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
+                  uint32_t iterMax, double R, int dtype, int scheme, int ngpus, uint32_t* out_u32) {
+    if (!out_u32) return fail(MANDEL_EINVAL, "out_u32 must not be NULL");
+    return mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iterMax, R, dtype, scheme, ngpus,
+                            nullptr, out_u32, nullptr, nullptr, nullptr);
+}
+
+int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
+                       uint32_t iterMax, double R, int dtype, int scheme, int rank, int nranks,
+                       const mandel_options* opts, uint32_t* out_root, uint32_t* fcfs_counter,
+                       void* streamv, mandel_stats* stats) {
+    BusyGuard busy;
+    if (!busy.ok) return fail(MANDEL_EBUSY, "another mandel call is in progress");
+    std::lock_guard<std::mutex> lk(g_mu);
+    Derived d;
+    int rc = derive(xmin, xmax, ymin, ymax, W, H, iterMax, R, dtype, d);
+    if (rc) return rc;
+    if (scheme < MANDEL_BLOCK || scheme > MANDEL_FCFS) return fail(MANDEL_EINVAL, "scheme out of range");
+    if (nranks < 1 || nranks > MANDEL_MAX_GPUS || rank < 0 || rank >= nranks)
+        return fail(MANDEL_EINVAL, "rank/nranks out of range");
+    if (!out_root) return fail(MANDEL_EINVAL, "out_root must not be NULL");
+    if (scheme == MANDEL_FCFS && !fcfs_counter) return fail(MANDEL_EINVAL, "FCFS needs fcfs_counter");
+    if (scheme != MANDEL_FCFS && H < (uint32_t)nranks) return fail(MANDEL_EINVAL, "static schemes need H >= nranks");
+    int ndev = 0;
+    rc = device_count(ndev);
+    if (rc) return rc;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    rc = ensure_device(dev);
+    if (rc) return rc;
+    const size_t sbytes = state_bytes_for(H, opts);
+    // slot 0 of the rank table holds this process's single rank
+    rc = ensure_rank(0, dev, sbytes, nullptr);
+    if (rc) return rc;
+    RankCtx& rk = g_rank[0];
+    LaunchSpec ls;
+    rc = build_params(d, W, H, iterMax, dtype, scheme, nranks, rank, opts, out_root, rk.state,
+                      fcfs_counter, dev, ls);
+    if (rc) return rc;
+    cudaStream_t s = streamv ? (cudaStream_t)streamv : rk.stream;
+    const double t0 = now_ms();
+    CK(cudaMemsetAsync(rk.state, 0, sbytes, s));
+    CK(cudaEventRecord(rk.k0, s));
+    rc = launch(ls, s);
+    if (rc) return rc;
+    CK(cudaEventRecord(rk.k1, s));
+    mandel::WorkState ws;
+    CK(cudaMemcpyAsync(&ws, rk.state, sizeof(ws), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, rk.k0, rk.k1));
+        stats->kernel_ms[0] = ms;
+        stats->kernel_ms_max = ms;
+        stats->device_ms = ms;
+        stats->rank_iters[0] = ws.sum_iters;
+        stats->rank_pixels[0] = ws.pixels;
+        stats->rank_rows[0] = ws.rows_started;
+        stats->sum_iters = ws.sum_iters;
+        stats->pixels = ws.pixels;
+        stats->chunks_claimed = ws.chunks_claimed;
+        stats->transfers = rank == 0 ? 0u : (scheme == MANDEL_FCFS ? ws.chunks_claimed : 1u);
+        stats->kernel_launches = 1;
+        stats->ngpus = 1;
+        stats->ndevices = 1;
+        stats->total_ms = now_ms() - t0;
+    }
+    return MANDEL_OK;
+}
+
+int mandel_dev_alloc(int device, size_t bytes, void** dev_ptr) {
+    if (!dev_ptr || bytes == 0) return fail(MANDEL_EINVAL, "dev_alloc needs a pointer and bytes > 0");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CK(cudaSetDevice(device));
+    cudaError_t e = cudaMalloc(dev_ptr, bytes);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    return MANDEL_OK;
+}
+
+int mandel_dev_free(void* dev_ptr) {
+    if (!dev_ptr) return MANDEL_OK;
+    CK(cudaFree(dev_ptr));
+    return MANDEL_OK;
+}
+
+int mandel_ipc_handle(void* dev_ptr, void* handle_out) {
+    if (!dev_ptr || !handle_out) return fail(MANDEL_EINVAL, "ipc_handle needs pointers");
+    static_assert(sizeof(cudaIpcMemHandle_t) == MANDEL_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+    if (e != cudaSuccess) { cuda_fail(e, "cudaIpcGetMemHandle"); return MANDEL_ECOMM; }
+    std::memcpy(handle_out, &h, sizeof(h));
+    return MANDEL_OK;
+}
+
+int mandel_ipc_open(const void* handle, void** dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return fail(MANDEL_EINVAL, "ipc_open needs pointers");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) { cuda_fail(e, "cudaIpcOpenMemHandle"); return MANDEL_ECOMM; }
+    return MANDEL_OK;
+}
+
+int mandel_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return fail(MANDEL_EINVAL, "ipc_close needs a pointer");
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) { cuda_fail(e, "cudaIpcCloseMemHandle"); return MANDEL_ECOMM; }
+    return MANDEL_OK;
+}
+
+int mandel_dev_zero(void* dev_ptr, size_t bytes, void* stream) {
+    if (!dev_ptr) return fail(MANDEL_EINVAL, "dev_zero needs a pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(dev_ptr, 0, bytes, s));
+    CK(cudaStreamSynchronize(s));
+    return MANDEL_OK;
+}
+
+void mandel_shutdown(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int r = 0; r < MANDEL_MAX_GPUS; ++r) {
+        RankCtx& rc = g_rank[r];
+        if (rc.device < 0) continue;
+        cudaSetDevice(rc.device);
+        if (rc.stream) cudaStreamDestroy(rc.stream);
+        if (rc.k0) cudaEventDestroy(rc.k0);
+        if (rc.k1) cudaEventDestroy(rc.k1);
+        if (rc.state) cudaFree(rc.state);
+        rc = RankCtx();
+    }
+    if (!g_dev.empty()) {
+        cudaSetDevice(0);
+        if (g_root.image) cudaFree(g_root.image);
+        if (g_root.fcfs_ctr) cudaFree(g_root.fcfs_ctr);
+        if (g_root.start) cudaEventDestroy(g_root.start);
+        if (g_root.done) cudaEventDestroy(g_root.done);
+        if (g_root.d2h) cudaEventDestroy(g_root.d2h);
+    }
+    g_root = Root();
+    for (auto& d : g_dev) d.init = false;
+    cudaGetLastError();
+}
+
+}  // extern "C"

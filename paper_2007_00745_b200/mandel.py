@@ -1,0 +1,277 @@
+"""Thin ctypes binding of libmandel.so (include/mandel.h), same names as the C ABI.
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  There is no CPU fallback -- if the shared library is missing or
+fails to load this module raises, and on a machine without a CUDA device the
+compute calls return MANDEL_ENODEV (raised as MandelError).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmandel.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "mandel.h")
+
+MANDEL_FP64, MANDEL_FP32 = 0, 1
+MANDEL_BLOCK, MANDEL_CYCLIC, MANDEL_FCFS = 0, 1, 2
+MANDEL_OK, MANDEL_EINVAL, MANDEL_ENODEV, MANDEL_ENOMEM = 0, -1, -2, -3
+MANDEL_ECUDA, MANDEL_ECOMM, MANDEL_EBUSY = -4, -5, -6
+MANDEL_KERNEL_REFILL, MANDEL_KERNEL_STATIC = 0, 1
+MANDEL_MAX_GPUS = 64
+MANDEL_IPC_HANDLE_BYTES = 64
+
+DTYPES = {"fp64": MANDEL_FP64, "fp32": MANDEL_FP32}
+SCHEMES = {"block": MANDEL_BLOCK, "naive": MANDEL_BLOCK, "cyclic": MANDEL_CYCLIC,
+           "alternating": MANDEL_CYCLIC, "fcfs": MANDEL_FCFS}
+
+
+class MandelError(RuntimeError):
+    def __init__(self, code: int, where: str, detail: str = ""):
+        self.code = code
+        super().__init__(f"{where}: {strerror(code)} ({code}) {detail}".strip())
+
+
+class mandel_stats(ctypes.Structure):
+    _fields_ = [
+        ("device_ms", ctypes.c_double),
+        ("kernel_ms_max", ctypes.c_double),
+        ("kernel_ms", ctypes.c_double * MANDEL_MAX_GPUS),
+        ("d2h_ms", ctypes.c_double),
+        ("total_ms", ctypes.c_double),
+        ("sum_iters", ctypes.c_uint64),
+        ("pixels", ctypes.c_uint64),
+        ("rank_iters", ctypes.c_uint64 * MANDEL_MAX_GPUS),
+        ("rank_pixels", ctypes.c_uint64 * MANDEL_MAX_GPUS),
+        ("rank_rows", ctypes.c_uint32 * MANDEL_MAX_GPUS),
+        ("chunks_claimed", ctypes.c_uint32),
+        ("transfers", ctypes.c_uint32),
+        ("kernel_launches", ctypes.c_uint32),
+        ("ngpus", ctypes.c_uint32),
+        ("ndevices", ctypes.c_uint32),
+    ]
+
+    def as_dict(self) -> dict:
+        n = max(int(self.ngpus), 1)
+        return {
+            "device_ms": self.device_ms, "kernel_ms_max": self.kernel_ms_max,
+            "kernel_ms": list(self.kernel_ms[:n]), "d2h_ms": self.d2h_ms,
+            "total_ms": self.total_ms, "sum_iters": int(self.sum_iters),
+            "pixels": int(self.pixels), "rank_iters": [int(v) for v in self.rank_iters[:n]],
+            "rank_pixels": [int(v) for v in self.rank_pixels[:n]],
+            "rank_rows": [int(v) for v in self.rank_rows[:n]],
+            "chunks_claimed": int(self.chunks_claimed), "transfers": int(self.transfers),
+            "kernel_launches": int(self.kernel_launches), "ngpus": int(self.ngpus),
+            "ndevices": int(self.ndevices),
+        }
+
+
+class mandel_options(ctypes.Structure):
+    _fields_ = [
+        ("chunk_rows", ctypes.c_uint32),
+        ("tile_px", ctypes.c_uint32),
+        ("kernel", ctypes.c_int),
+        ("logical_ranks", ctypes.c_int),
+        ("reserved", ctypes.c_int * 4),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+_SCALARS = [ctypes.c_double] * 4 + [ctypes.c_uint32] * 3 + [ctypes.c_double]
+
+
+def lib():
+    """Load libmandel.so; raise if it is missing (no fallback path exists)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                                  "(the CUDA library is the only implementation)")
+            L = ctypes.CDLL(LIB_PATH)
+            i32, u32, vp = ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p
+            L.mandel_render.argtypes = _SCALARS + [i32, i32, i32, vp]
+            L.mandel_render.restype = i32
+            L.mandel_render_ex.argtypes = _SCALARS + [i32, i32, i32, vp, vp, vp, vp, vp]
+            L.mandel_render_ex.restype = i32
+            L.mandel_render_rank.argtypes = _SCALARS + [i32, i32, i32, i32, vp, vp, vp, vp, vp]
+            L.mandel_render_rank.restype = i32
+            L.mandel_plan_rows.argtypes = [i32, u32, i32, i32, vp, vp]
+            L.mandel_plan_rows.restype = i32
+            L.mandel_strerror.argtypes = [i32]
+            L.mandel_strerror.restype = ctypes.c_char_p
+            L.mandel_last_error.argtypes = []
+            L.mandel_last_error.restype = ctypes.c_char_p
+            L.mandel_device_count.argtypes = []
+            L.mandel_device_count.restype = i32
+            L.mandel_shutdown.argtypes = []
+            L.mandel_shutdown.restype = None
+            L.mandel_abi_version.argtypes = []
+            L.mandel_abi_version.restype = i32
+            L.mandel_dev_alloc.argtypes = [i32, ctypes.c_size_t, vp]
+            L.mandel_dev_alloc.restype = i32
+            L.mandel_dev_free.argtypes = [vp]
+            L.mandel_dev_free.restype = i32
+            L.mandel_ipc_handle.argtypes = [vp, vp]
+            L.mandel_ipc_handle.restype = i32
+            L.mandel_ipc_open.argtypes = [vp, vp]
+            L.mandel_ipc_open.restype = i32
+            L.mandel_dev_zero.argtypes = [vp, ctypes.c_size_t, vp]
+            L.mandel_dev_zero.restype = i32
+            L.mandel_ipc_close.argtypes = [vp]
+            L.mandel_ipc_close.restype = i32
+            _lib = L
+    return _lib
+
+
+def header_symbols() -> list[str]:
+    """Function names include/mandel.h declares (for the export test)."""
+    text = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(mandel_\w+)\s*\(", text, re.M)))
+
+
+def strerror(code: int) -> str:
+    return lib().mandel_strerror(code).decode()
+
+
+def last_error() -> str:
+    return lib().mandel_last_error().decode()
+
+
+def _check(rc: int, where: str):
+    if rc != MANDEL_OK:
+        raise MandelError(rc, where, last_error())
+
+
+def _enum(v, table):
+    return table[v] if isinstance(v, str) else int(v)
+
+
+def _ptr(a) -> int | None:
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    raise TypeError(f"cannot take a pointer of {type(a)}")
+
+
+def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False):
+    o = mandel_options()
+    o.chunk_rows = chunk_rows or 0
+    o.tile_px = tile_px or 0
+    o.kernel = kernel
+    o.logical_ranks = 1 if logical_ranks else 0
+    return o
+
+
+def mandel_device_count() -> int:
+    return int(lib().mandel_device_count())
+
+
+def mandel_abi_version() -> int:
+    return int(lib().mandel_abi_version())
+
+
+def mandel_shutdown() -> None:
+    lib().mandel_shutdown()
+
+
+def mandel_render(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, ngpus, out) -> None:
+    """C: mandel_render.  ``out``: host numpy uint32 array (or torch CPU tensor) of W*H."""
+    rc = lib().mandel_render(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
+                             _enum(scheme, SCHEMES), ngpus, _ptr(out))
+    _check(rc, "mandel_render")
+
+
+def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", scheme="block",
+                     ngpus=1, *, out_host=None, out_dev0=None, stream0=None, chunk_rows=0,
+                     tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False) -> dict:
+    """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
+    device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
+    Returns the call's statistics as a dict."""
+    st = mandel_stats()
+    o = _opts(chunk_rows, tile_px, kernel, logical_ranks)
+    rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
+                                _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
+                                _ptr(out_dev0), stream0, ctypes.byref(st))
+    _check(rc, "mandel_render_ex")
+    return st.as_dict()
+
+
+def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, rank, nranks,
+                       out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
+                       kernel=MANDEL_KERNEL_REFILL) -> dict:
+    """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
+    pointers valid in this process (own, or mapped with mandel_ipc_open)."""
+    st = mandel_stats()
+    o = _opts(chunk_rows, tile_px, kernel, False)
+    rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
+                                  _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
+                                  _ptr(out_root), _ptr(fcfs_counter), stream, ctypes.byref(st))
+    _check(rc, "mandel_render_rank")
+    return st.as_dict()
+
+
+def mandel_plan_rows(scheme, H: int, ngpus: int, rank: int) -> np.ndarray:
+    """C: mandel_plan_rows (host-only planner of the static schemes)."""
+    L = lib()
+    cnt = ctypes.c_uint32(0)
+    _check(L.mandel_plan_rows(_enum(scheme, SCHEMES), H, ngpus, rank, None, ctypes.byref(cnt)),
+           "mandel_plan_rows")
+    rows = np.zeros(cnt.value, dtype=np.uint32)
+    _check(L.mandel_plan_rows(_enum(scheme, SCHEMES), H, ngpus, rank,
+                              rows.ctypes.data if cnt.value else None, ctypes.byref(cnt)),
+           "mandel_plan_rows")
+    return rows
+
+
+def mandel_dev_alloc(device: int, nbytes: int) -> int:
+    p = ctypes.c_void_p(0)
+    _check(lib().mandel_dev_alloc(device, nbytes, ctypes.byref(p)), "mandel_dev_alloc")
+    return int(p.value)
+
+
+def mandel_dev_free(ptr: int) -> None:
+    _check(lib().mandel_dev_free(ptr), "mandel_dev_free")
+
+
+def mandel_dev_zero(ptr: int, nbytes: int, stream=None) -> None:
+    _check(lib().mandel_dev_zero(ptr, nbytes, stream), "mandel_dev_zero")
+
+
+def mandel_ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(MANDEL_IPC_HANDLE_BYTES)
+    _check(lib().mandel_ipc_handle(ptr, buf), "mandel_ipc_handle")
+    return buf.raw
+
+
+def mandel_ipc_open(handle: bytes) -> int:
+    if len(handle) != MANDEL_IPC_HANDLE_BYTES:
+        raise ValueError("IPC handle must be MANDEL_IPC_HANDLE_BYTES long")
+    p = ctypes.c_void_p(0)
+    _check(lib().mandel_ipc_open(handle, ctypes.byref(p)), "mandel_ipc_open")
+    return int(p.value)
+
+
+def mandel_ipc_close(ptr: int) -> None:
+    _check(lib().mandel_ipc_close(ptr), "mandel_ipc_close")
+
+
+def render(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", scheme="block", ngpus=1,
+           **kw):
+    """Convenience: the map as a (H, W) numpy uint32 array plus the stats dict."""
+    out = np.zeros((H, W), dtype=np.uint32)
+    st = mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, ngpus,
+                          out_host=out, **kw)
+    return out, st

@@ -1,0 +1,90 @@
+"""The C-ABI boundary without a GPU: the library loads, exports every symbol the
+header declares, validates arguments (EINVAL before any device work), and
+reports ENODEV instead of falling back to the CPU when no device is present."""
+import ctypes
+import math
+import subprocess
+
+import numpy as np
+import pytest
+
+import workloads as wl
+
+
+def test_exports_every_header_symbol(mandel):
+    names = mandel.header_symbols()
+    assert "mandel_render" in names and "mandel_plan_rows" in names and len(names) >= 14
+    L = mandel.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    # and the dynamic symbol table really has them (extern "C", unmangled)
+    out = subprocess.run(["nm", "-D", "--defined-only", mandel.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    for n in names:
+        assert f" T {n}\n" in out or out.endswith(f" T {n}"), n
+
+
+def test_library_is_sm100a_only(mandel):
+    out = subprocess.run(["cuobjdump", "--list-elf", mandel.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", mandel.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    # no FMA contraction anywhere in the escape kernels (bit-exactness, R10)
+    for line in sass.splitlines():
+        assert "DFMA" not in line and "FFMA" not in line, line
+
+
+def test_abi_version_and_strerror(mandel):
+    assert mandel.mandel_abi_version() == 1
+    for code in range(-6, 1):
+        assert mandel.strerror(code) and mandel.strerror(code) != "unknown status"
+
+
+def _call(mandel, **kw):
+    a = dict(xmin=-2.5, xmax=1.5, ymin=-2.0, ymax=2.0, W=8, H=8, iter_max=10, R=2.0,
+             dtype=0, scheme=0, ngpus=1)
+    a.update(kw)
+    out = np.zeros(max(a["W"] * a["H"], 1), dtype=np.uint32)
+    return mandel.lib().mandel_render(a["xmin"], a["xmax"], a["ymin"], a["ymax"], a["W"], a["H"],
+                                      a["iter_max"], a["R"], a["dtype"], a["scheme"], a["ngpus"],
+                                      out.ctypes.data)
+
+
+BAD_ARGS = [
+    dict(W=0), dict(H=0), dict(iter_max=0), dict(R=0.0), dict(R=-1.0), dict(R=math.inf),
+    dict(R=1e200), dict(xmin=math.nan), dict(ymax=math.inf), dict(xmin=1.5), dict(ymin=2.0),
+    dict(dtype=2), dict(dtype=-1), dict(scheme=3), dict(H=3, ngpus=4),
+    dict(dtype=1, R=1e20), dict(dtype=1, xmin=-1e39), dict(dtype=1, xmin=1.0, xmax=1.0 + 1e-12),
+    dict(W=0xFFFFFFFF, H=0xFFFFFFFF) if ctypes.sizeof(ctypes.c_size_t) == 4 else dict(W=0),
+]
+
+
+@pytest.mark.parametrize("kw", BAD_ARGS)
+def test_einval(mandel, kw):
+    assert _call(mandel, **kw) == mandel.MANDEL_EINVAL, kw
+    assert mandel.last_error()
+
+
+def test_null_outputs_rejected(mandel):
+    L = mandel.lib()
+    rc = L.mandel_render(-2.5, 1.5, -2.0, 2.0, 8, 8, 10, 2.0, 0, 0, 1, None)
+    assert rc == mandel.MANDEL_EINVAL
+    rc = L.mandel_render_ex(-2.5, 1.5, -2.0, 2.0, 8, 8, 10, 2.0, 0, 0, 1, None, None, None,
+                            None, None)
+    assert rc == mandel.MANDEL_EINVAL
+    rc = L.mandel_render_rank(-2.5, 1.5, -2.0, 2.0, 8, 8, 10, 2.0, 0, 0, 0, 1, None, None,
+                              None, None, None)
+    assert rc == mandel.MANDEL_EINVAL
+    rc = L.mandel_render_rank(-2.5, 1.5, -2.0, 2.0, 8, 8, 10, 2.0, 0, 0, 2, 2, None,
+                              ctypes.c_void_p(16), None, None, None)
+    assert rc == mandel.MANDEL_EINVAL
+
+
+def test_no_device_means_enodev_not_fallback(mandel):
+    if mandel.mandel_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    assert _call(mandel) == mandel.MANDEL_ENODEV
+    with pytest.raises(mandel.MandelError) as e:
+        mandel.render(*wl.C1.args())
+    assert e.value.code == mandel.MANDEL_ENODEV

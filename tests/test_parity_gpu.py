@@ -1,0 +1,199 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, on a B200.
+
+Integer outputs: the bar is bit-exact equality, element by element (DESIGN.md
+"Parity").  Small maps are compared whole; the full-size configurations, in the
+launch configuration bench.py times, are compared on seeded sampled rows the
+oracle computes one by one, plus properties that hold at any size (range,
+coverage, exact mirror rows, power-of-two decimation against a whole oracle map,
+Σcounts against the map).
+"""
+import numpy as np
+import pytest
+
+import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+SCHEMES = ["block", "cyclic", "fcfs"]
+
+
+def _torch():
+    import torch
+    assert torch.cuda.is_available(), "gpu test without a CUDA device"
+    return torch
+
+
+def _render_dev(mandel, cfg, scheme="block", ngpus=1, **kw):
+    torch = _torch()
+    out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device="cuda:0")
+    st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, ngpus, out_dev0=out,
+                                 logical_ranks=ngpus > 1, **kw)
+    return out, st
+
+
+def _host(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _assert_same(got, want, label):
+    if not np.array_equal(got, want):
+        bad = np.argwhere(got != want)
+        i, j = bad[0]
+        raise AssertionError(f"{label}: {len(bad)} pixels differ; first at (i={i}, j={j}): "
+                             f"gpu={got[i, j]} oracle={want[i, j]}")
+
+
+# ---------------------------------------------------------------------------
+# whole maps: C1 and reduced shapes, every scheme, logical rank counts, kernels
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("ngpus", [1, 2, 3, 5, 8])
+def test_c1_all_schemes(mandel, oracle, dtype, scheme, ngpus):
+    cfg = wl.C1.with_(dtype=dtype)
+    want = oracle.render(cfg)
+    out, st = _render_dev(mandel, cfg, scheme, ngpus)
+    _assert_same(_host(out), want, f"C1/{dtype}/{scheme}/N={ngpus}")
+    assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
+    assert st["pixels"] == cfg.pixels
+    assert st["kernel_launches"] == ngpus
+    if scheme == "fcfs":
+        assert st["chunks_claimed"] == -(-cfg.H // 16)  # Eq. 19 analog: ceil(H/16) claims
+    else:
+        assert st["transfers"] == ngpus - 1  # Eq. 18 / Eq. 20: T_m = N - 1
+        assert st["rank_rows"] == [len(x) for x in (
+            mandel.mandel_plan_rows(scheme, cfg.H, ngpus, r) for r in range(ngpus))]
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("scheme", ["block", "cyclic"])
+def test_static_kernel_variant(mandel, oracle, dtype, scheme):
+    cfg = wl.C1.with_(dtype=dtype, W=813, H=611)
+    out, st = _render_dev(mandel, cfg, scheme, 3, kernel=mandel.MANDEL_KERNEL_STATIC)
+    _assert_same(_host(out), oracle.render(cfg), f"static/{dtype}/{scheme}")
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_random_small_configs(mandel, oracle, dtype):
+    for k, cfg in enumerate(wl.random_small_configs(50, 0, dtype)):
+        want = oracle.render(cfg)
+        scheme = SCHEMES[k % 3]
+        ngpus = [1, 2, 3, 4, 5, 8][k % 6]
+        if scheme != "fcfs" and cfg.H < ngpus:
+            ngpus = 1
+        out, st = _render_dev(mandel, cfg, scheme, ngpus, tile_px=[0, 1, 7, 32, 33][k % 5],
+                              chunk_rows=[0, 1, 3][k % 3])
+        _assert_same(_host(out), want, f"{cfg.name}/{dtype}/{scheme}/N={ngpus}")
+        assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
+
+
+EDGE = [
+    wl.Config("1x1", -2.5, 1.5, -2.0, 2.0, 1, 1, 50, 2.0, "fp64"),
+    wl.Config("1xH", -0.8, -0.7, -0.2, 0.2, 1, 97, 300, 2.0, "fp64"),
+    wl.Config("Wx1", -2.5, 1.5, 0.0, 0.01, 1025, 1, 300, 2.0, "fp64"),
+    wl.Config("ragged", -2.2, 0.8, -1.3, 1.1, 257, 33, 500, 2.0, "fp64"),
+    wl.Config("it1", -2.5, 1.5, -2.0, 2.0, 64, 64, 1, 2.0, "fp64"),
+    wl.Config("it2", -2.5, 1.5, -2.0, 2.0, 64, 64, 2, 2.0, "fp32"),
+    wl.Config("far", -1e300, 1e300, -1e300, 1e300, 40, 40, 100, 2.0, "fp64"),
+    wl.Config("R20", -2.5, 1.5, -2.0, 2.0, 120, 90, 2000, 20.0, "fp64"),
+    wl.Config("Rsmall", -1.0, 0.5, -0.7, 0.7, 100, 100, 400, 0.75, "fp32"),
+    wl.Config("tiny", -0.7436439, -0.7436438, 0.1318259, 0.131826, 64, 64, 3000, 2.0, "fp64"),
+]
+
+
+@pytest.mark.parametrize("cfg", EDGE, ids=[c.name for c in EDGE])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_edge_cases(mandel, oracle, cfg, scheme):
+    want = oracle.render(cfg)
+    for ngpus in (1, 4):
+        if scheme != "fcfs" and cfg.H < ngpus:
+            continue
+        out, st = _render_dev(mandel, cfg, scheme, ngpus)
+        got = _host(out)
+        _assert_same(got, want, f"{cfg.name}/{scheme}/N={ngpus}")
+        assert got.min() >= 1 and got.max() <= cfg.iter_max
+        assert st["pixels"] == cfg.pixels
+
+
+def test_fcfs_more_ranks_than_rows(mandel, oracle):
+    cfg = wl.Config("fewrows", -2.5, 1.5, -2.0, 2.0, 300, 3, 200, 2.0, "fp64")
+    out, st = _render_dev(mandel, cfg, "fcfs", 8, chunk_rows=1)
+    _assert_same(_host(out), oracle.render(cfg), "fcfs N>H")
+    assert st["chunks_claimed"] == 3
+
+
+def test_host_output_entry_point(mandel, oracle):
+    cfg = wl.C1.with_(W=640, H=480)
+    out = np.zeros(cfg.pixels, dtype=np.uint32)
+    mandel.mandel_render(*cfg.args(), "fp64", "cyclic", 1, out)
+    _assert_same(out.reshape(cfg.H, cfg.W), oracle.render(cfg), "mandel_render host out")
+    got, st = mandel.render(*cfg.args(), "fp32", "fcfs", 1)
+    _assert_same(got, oracle.render(cfg.with_(dtype="fp32")), "render fp32")
+    assert st["d2h_ms"] > 0
+
+
+def test_repeat_is_deterministic(mandel):
+    cfg = wl.C1.with_(iter_max=1000)
+    a, _ = _render_dev(mandel, cfg, "fcfs", 1)
+    for scheme, n in (("fcfs", 3), ("block", 1), ("cyclic", 4), ("fcfs", 1)):
+        b, _ = _render_dev(mandel, cfg, scheme, n)
+        assert bool((a == b).all()), (scheme, n)
+
+
+# ---------------------------------------------------------------------------
+# full-size configurations, in bench.py's launch configuration (1 GPU, FCFS)
+# ---------------------------------------------------------------------------
+def _sampled_rows_check(oracle, cfg, out, nrows, seed):
+    rows = wl.sample_rows(cfg.H, nrows, seed, include=(0, 1, cfg.H // 2 - 1))
+    got = _host(out[rows.tolist()])
+    want, _ = oracle.render_rows_mt(cfg, rows)
+    _assert_same(got, want, f"{cfg.name} sampled rows")
+
+
+def _properties(oracle, cfg, out, st):
+    torch = _torch()
+    assert int(out.min()) >= 1 and int(out.max()) <= cfg.iter_max  # coverage of a 0-prefill
+    total = int(out.to(torch.int64).sum())
+    assert st["sum_iters"] == total
+    assert st["pixels"] == cfg.pixels
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,nrows", [("C2", 48), ("C3", 48), ("C4", 16)])
+def test_full_size_sampled(mandel, oracle, name, nrows):
+    cfg = wl.CONFIGS[name]
+    out, st = _render_dev(mandel, cfg, "fcfs", 1)
+    _properties(oracle, cfg, out, st)
+    _sampled_rows_check(oracle, cfg, out, nrows, seed=sum(map(ord, name)))
+    if name in ("C2", "C3"):
+        # exact mirror rows (rows i and H-i with bitwise-opposite Cy are identical)
+        _, cy = oracle.axes(*cfg.args()[:4], 1, cfg.H, cfg.R, cfg.dtype)
+        pairs = [(i, cfg.H - i) for i in range(1, cfg.H) if cy[i] == -cy[cfg.H - i]]
+        assert len(pairs) > 100
+        a = out[[p[0] for p in pairs]]
+        b = out[[p[1] for p in pairs]]
+        assert bool((a == b).all())
+
+
+@pytest.mark.slow
+def test_c5_decimation_and_rows(mandel, oracle):
+    torch = _torch()
+    cfg = wl.C5
+    out, st = _render_dev(mandel, cfg, "fcfs", 1)
+    _properties(oracle, cfg, out, st)
+    # c is an exact dyadic on 32768^2 over [-2.5,1.5]x[-2,2]: every 32nd pixel is the 1024^2 map
+    small = wl.Config("C5/32", *wl.FULL_PLANE, 1024, 1024, cfg.iter_max, cfg.R, "fp64")
+    want, _ = oracle.render_rows_mt(small, np.arange(1024))
+    _assert_same(_host(out[::32, ::32].contiguous()), want, "C5[::32, ::32]")
+    _sampled_rows_check(oracle, cfg, out, 12, seed=5)
+    del out
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_c2_schemes_agree(mandel, scheme):
+    ref, _ = _render_dev(mandel, wl.C2, "fcfs", 1)
+    out, st = _render_dev(mandel, wl.C2, scheme, 8)
+    assert bool((ref == out).all())
+    assert st["pixels"] == wl.C2.pixels
