@@ -73,8 +73,11 @@ enum mandel_status {
 };
 
 enum mandel_kernel {
-    MANDEL_KERNEL_REFILL = 0,  /* persistent CTAs, per-warp tile queue, lane refill (default) */
-    MANDEL_KERNEL_STATIC = 1   /* one pixel per thread, static grid (baseline; BLOCK/CYCLIC only) */
+    MANDEL_KERNEL_REFILL = 0,  /* default: the fastest measured configuration for the dtype      */
+    MANDEL_KERNEL_STATIC = 1,  /* one pixel per thread, static grid (baseline; BLOCK/CYCLIC only)  */
+    MANDEL_KERNEL_EAGER = 2,   /* persistent CTAs, warp tile queue, lane refill on every escape   */
+    MANDEL_KERNEL_LAZY = 3     /* the same, refill batched: escapes recorded in-loop, the warp
+                                  refills when refill_lanes lanes hold a finished pixel          */
 };
 
 /* Per-call statistics (all fields written when stats != NULL and the call succeeds). */
@@ -104,7 +107,11 @@ typedef struct mandel_options {
     int      kernel;         /* enum mandel_kernel                                                */
     int      logical_ranks;  /* nonzero: allow ngpus > device count, rank g runs on device
                                 g % count on its own stream (tests; ranks never wait on each other) */
-    int      reserved[4];
+    int      refill_lanes;   /* LAZY: lanes with a finished pixel that trigger a refill (1..32);
+                                0 -> library default                                               */
+    int      ilp;            /* EAGER/LAZY: pixels per lane (EAGER 1..4, LAZY 1..2); 0 -> default  */
+    int      min_ctas;       /* EAGER/LAZY: register budget as CTAs per SM (1,4,5,6,8); 0 -> default */
+    int      reserved;
 } mandel_options;
 
 /*

@@ -139,8 +139,7 @@ int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
 struct DeviceCtx {
     bool init = false;
     int sms = 0;
-    int occ_refill[2] = {0, 0};  // CTAs/SM, [fp64, fp32]
-    int occ_static[2] = {0, 0};
+    int occ_cache[2][4][5][5] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
     bool peer_to0 = false;
 };
 
@@ -171,6 +170,47 @@ struct BusyGuard {
     ~BusyGuard() { if (ok) g_busy.store(false); }
 };
 
+typedef void (*KernelFn)(mandel::Params);
+
+// Register-budget instantiations (min CTAs per SM in __launch_bounds__).
+constexpr int kMinbVals[5] = {1, 4, 5, 6, 8};
+int minb_index(int v) {
+    for (int i = 0; i < 5; ++i)
+        if (kMinbVals[i] == v) return i;
+    return -1;
+}
+
+#define MANDEL_MINB_ROW(K, T, I) \
+    {K<T, I, 1>, K<T, I, 4>, K<T, I, 5>, K<T, I, 6>, K<T, I, 8>}
+
+// kernel_fn(fp32, variant, ilp, minb index); nullptr if not instantiated.
+KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
+    using namespace mandel;
+    static const KernelFn eager[2][4][5] = {
+        {MANDEL_MINB_ROW(escape_refill_kernel, double, 1), MANDEL_MINB_ROW(escape_refill_kernel, double, 2),
+         MANDEL_MINB_ROW(escape_refill_kernel, double, 3), MANDEL_MINB_ROW(escape_refill_kernel, double, 4)},
+        {MANDEL_MINB_ROW(escape_refill_kernel, float, 1), MANDEL_MINB_ROW(escape_refill_kernel, float, 2),
+         MANDEL_MINB_ROW(escape_refill_kernel, float, 3), MANDEL_MINB_ROW(escape_refill_kernel, float, 4)},
+    };
+    static const KernelFn lazy[2][2][5] = {
+        {MANDEL_MINB_ROW(escape_lazy_kernel, double, 1), MANDEL_MINB_ROW(escape_lazy_kernel, double, 2)},
+        {MANDEL_MINB_ROW(escape_lazy_kernel, float, 1), MANDEL_MINB_ROW(escape_lazy_kernel, float, 2)},
+    };
+    if (variant == MANDEL_KERNEL_STATIC) return fp32 ? escape_static_kernel<float> : escape_static_kernel<double>;
+    if (mi < 0 || mi > 4) return nullptr;
+    if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
+    if (variant == MANDEL_KERNEL_LAZY && ilp >= 1 && ilp <= 2) return lazy[fp32][ilp - 1][mi];
+    return nullptr;
+}
+
+// MANDEL_KERNEL_REFILL resolves to these configurations (the measured fastest).
+struct KernelChoice {
+    int variant, ilp, minb;
+};
+constexpr KernelChoice kDefaultChoice[2] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp64: C2 75.6%, C5 84.4%
+                                            {MANDEL_KERNEL_EAGER, 4, 1}};  // fp32: C3 53.8% (issue-bound)
+constexpr uint32_t kDefaultRefillLanes = 8;
+
 int device_count(int& n) {
     n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
@@ -188,10 +228,6 @@ int ensure_device(int dev) {
     if (d.init) return MANDEL_OK;
     CK(cudaSetDevice(dev));
     CK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_refill[0], mandel::escape_refill_kernel<double>, mandel::kCtaThreads, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_refill[1], mandel::escape_refill_kernel<float>, mandel::kCtaThreads, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_static[0], mandel::escape_static_kernel<double>, mandel::kCtaThreads, 0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_static[1], mandel::escape_static_kernel<float>, mandel::kCtaThreads, 0));
     d.init = true;
     return MANDEL_OK;
 }
@@ -245,9 +281,19 @@ constexpr uint32_t kDefaultChunk = 16;
 struct LaunchSpec {
     mandel::Params p;
     dim3 grid, block;
-    bool refill;
-    bool fp32;
+    KernelFn fn;
 };
+
+int occupancy(int device, int fp32, int variant, int ilp, int mi, KernelFn fn, int& occ) {
+    int& c = g_dev[device].occ_cache[fp32][variant][variant == MANDEL_KERNEL_STATIC ? 0 : ilp][mi < 0 ? 0 : mi];
+    if (c == 0) {
+        CK(cudaSetDevice(device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, fn, mandel::kCtaThreads, 0));
+        if (c <= 0) c = 1;
+    }
+    occ = c;
+    return MANDEL_OK;
+}
 
 int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
@@ -256,7 +302,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     int rc = make_plan(scheme, H, nranks, rank, pl);
     if (rc) return rc;
     const int kernel = o ? o->kernel : MANDEL_KERNEL_REFILL;
-    if (kernel != MANDEL_KERNEL_REFILL && kernel != MANDEL_KERNEL_STATIC)
+    if (kernel < MANDEL_KERNEL_REFILL || kernel > MANDEL_KERNEL_LAZY)
         return fail(MANDEL_EINVAL, "options.kernel out of range");
     if (kernel == MANDEL_KERNEL_STATIC && scheme == MANDEL_FCFS)
         return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
@@ -268,6 +314,9 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.xmin = d.xmin; p.ymax = d.ymax; p.dx = d.dx; p.dy = d.dy;
     p.xminf = d.xminf; p.ymaxf = d.ymaxf; p.dxf = d.dxf; p.dyf = d.dyf;
     p.r2bits = d.r2bits;
+    // candidate key threshold: fp64 -> high word of bits(R2)+1; fp32 -> bits(R2)+1 (exact)
+    p.r2cand = dtype == MANDEL_FP64 ? (int)(((unsigned long long)d.r2bits + 1ull) >> 32)
+                                    : (int)(d.r2bits + 1);
     p.W = W; p.H = H; p.iter_max = iter_max;
     p.scheme = (uint32_t)scheme;
     p.tile_w = tile;
@@ -287,11 +336,27 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.fcfs_ctr = fcfs_ctr;
     const DeviceCtx& dc = g_dev[device];
     const int fi = dtype == MANDEL_FP32 ? 1 : 0;
-    ls.fp32 = fi == 1;
-    ls.refill = kernel == MANDEL_KERNEL_REFILL;
-    ls.block = ls.refill ? dim3(mandel::kCtaThreads) : dim3(32, mandel::kWarpsPerCta);
-    if (ls.refill) {
-        int occ = dc.occ_refill[fi] > 0 ? dc.occ_refill[fi] : 1;
+    KernelChoice kc = kDefaultChoice[fi];
+    if (kernel != MANDEL_KERNEL_REFILL) {
+        kc.variant = kernel;
+        kc.ilp = (o && o->ilp) ? o->ilp : (kernel == MANDEL_KERNEL_LAZY ? 2 : 2);
+        kc.minb = (o && o->min_ctas) ? o->min_ctas : 1;
+    } else if (o && (o->ilp || o->min_ctas)) {
+        if (o->ilp) kc.ilp = o->ilp;
+        if (o->min_ctas) kc.minb = o->min_ctas;
+    }
+    const int mi = minb_index(kc.minb);
+    ls.fn = kernel_fn(fi, kc.variant, kc.ilp, mi);
+    if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
+    const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;
+    int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;
+    if (rl < 1 || rl > 32) return fail(MANDEL_EINVAL, "options.refill_lanes must be in 1..32");
+    p.refill_lanes = (uint32_t)rl;
+    ls.block = persistent ? dim3(mandel::kCtaThreads) : dim3(32, mandel::kWarpsPerCta);
+    if (persistent) {
+        int occ = 1;
+        int rc2 = occupancy(device, fi, kc.variant, kc.ilp, mi, ls.fn, occ);
+        if (rc2) return rc2;
         ls.grid = dim3((unsigned)(occ * dc.sms));
     } else {
         ls.grid = dim3((W + 31) / 32, (pl.nslots + mandel::kWarpsPerCta - 1) / mandel::kWarpsPerCta);
@@ -307,13 +372,7 @@ size_t state_bytes_for(uint32_t H, const mandel_options* o) {
 }
 
 int launch(const LaunchSpec& ls, cudaStream_t s) {
-    if (ls.refill) {
-        if (ls.fp32) mandel::escape_refill_kernel<float><<<ls.grid, ls.block, 0, s>>>(ls.p);
-        else mandel::escape_refill_kernel<double><<<ls.grid, ls.block, 0, s>>>(ls.p);
-    } else {
-        if (ls.fp32) mandel::escape_static_kernel<float><<<ls.grid, ls.block, 0, s>>>(ls.p);
-        else mandel::escape_static_kernel<double><<<ls.grid, ls.block, 0, s>>>(ls.p);
-    }
+    ls.fn<<<ls.grid, ls.block, 0, s>>>(ls.p);
     CK(cudaGetLastError());
     return MANDEL_OK;
 }

@@ -43,12 +43,14 @@ struct Params {
     double xmin, ymax, dx, dy;       // fp64 mapping constants (host-derived, step a1)
     float xminf, ymaxf, dxf, dyf;    // fp32 mapping constants
     long long r2bits;                // bit pattern of R2 in the working type
+    int r2cand;                      // candidate threshold: key(bits(R2) + 1) (see Arith::key)
     uint32_t W, H, iter_max;
     uint32_t scheme;
     uint32_t tile_w, tiles_per_row;
     // static schemes: slot s -> row s < count0 ? base0 + s*stride0 : base1 + (s - count0)
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
+    uint32_t refill_lanes;           // lazy refill: leave the loop when this many lanes are free
     uint32_t* out;                   // rank 0's image, row-major W per row (local or peer)
     WorkState* ws;                   // this rank's state (local memory)
     uint32_t* chunk_map;             // this rank's local->global chunk table (local memory)
@@ -63,6 +65,9 @@ template <> struct Arith<double> {
     static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
     static __device__ __forceinline__ long long bits(double v) { return __double_as_longlong(v); }
     static __device__ __forceinline__ double cvt(uint32_t v) { return __uint2double_rn(v); }
+    // 32-bit escape-candidate key: the high word of the bit pattern.  key(s) >= r2cand
+    // (= high word of bits(R2) + 1) is necessary for s > R2; exits verify exactly.
+    static __device__ __forceinline__ int key(double v) { return __double2hiint(v); }
     static __device__ __forceinline__ double xmin(const Params& p) { return p.xmin; }
     static __device__ __forceinline__ double ymax(const Params& p) { return p.ymax; }
     static __device__ __forceinline__ double dx(const Params& p) { return p.dx; }
@@ -75,6 +80,7 @@ template <> struct Arith<float> {
     static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
     static __device__ __forceinline__ int bits(float v) { return __float_as_int(v); }
     static __device__ __forceinline__ float cvt(uint32_t v) { return __uint2float_rn(v); }
+    static __device__ __forceinline__ int key(float v) { return __float_as_int(v); }  // exact
     static __device__ __forceinline__ float xmin(const Params& p) { return p.xminf; }
     static __device__ __forceinline__ float ymax(const Params& p) { return p.ymaxf; }
     static __device__ __forceinline__ float dx(const Params& p) { return p.dxf; }
@@ -91,6 +97,18 @@ template <> struct Arith<float> {
         x2 = A::mul(x, x);                                         \
         y2 = A::mul(y, y);                                         \
         esc = A::bits(A::add(x2, y2)) > r2;                        \
+    } while (0)
+
+// The same update on slot s of the per-lane arrays (refill kernel).
+#define MANDEL_STEP_SLOT(s)                                                \
+    do {                                                                   \
+        T ny_ = A::add(A::mul(A::add(x[s], x[s]), y[s]), ci[s]);           \
+        T nx_ = A::add(A::sub(x2[s], y2[s]), cr[s]);                       \
+        x[s] = nx_;                                                        \
+        y[s] = ny_;                                                        \
+        x2[s] = A::mul(x[s], x[s]);                                        \
+        y2[s] = A::mul(y[s], y[s]);                                        \
+        esc[s] = A::key(A::add(x2[s], y2[s])) >= r2c;                      \
     } while (0)
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
@@ -170,14 +188,16 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
 
 // ---------------------------------------------------------------------------
 // K1/K2: persistent escape kernel with a per-warp tile queue and lane refill.
-// Each warp runs the iteration warp-uniformly (no per-lane branch) and leaves
-// the inner loop as soon as any lane escapes or reaches iterMax; finished lanes
-// store their count and immediately take the next pixel of the warp's tile
-// stream, so lanes stay busy through the divergence near the set boundary.
-// Per-lane state: z (x, y), x2, y2, c (cr, ci), remaining iterations, output index.
+// Each lane holds ILP independent pixels ("slots"); their z-updates are
+// interleaved so the FP64 dependency chains of one warp overlap.  The warp
+// iterates warp-uniformly (no per-lane branch) and leaves the inner loop as
+// soon as any slot escapes or the smallest remaining budget runs out; finished
+// slots store their count and immediately take the next pixels of the warp's
+// tile stream, so lanes stay busy through the divergence near the set boundary.
+// Per-slot state: z (x, y), x2, y2, c (cr, ci), remaining iterations, output ptr.
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(kCtaThreads)
+template <typename T, int ILP, int MINB>
+__global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     typedef Arith<T> A;
     typedef typename A::bits_t B;
@@ -185,26 +205,44 @@ escape_refill_kernel(const Params p) {
     const uint32_t lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const B r2 = (B)p.r2bits;
+    const int r2c = p.r2cand;
     const T xmin = A::xmin(p), ymax = A::ymax(p), dx = A::dx(p), dy = A::dy(p);
     const T zero = T(0);
 
-    T x = zero, y = zero, x2 = zero, y2 = zero, cr = zero, ci = zero;
-    uint32_t rem = kIdleRem;
-    bool active = false;
-    uint32_t* dst = p.out;
+    // per-slot state; rem == kIdleRem marks an idle slot (z = c = 0: never a candidate)
+    T x[ILP], y[ILP], x2[ILP], y2[ILP], cr[ILP], ci[ILP];
+    uint32_t rem[ILP];
+    bool esc[ILP];
+    uint32_t* dst[ILP];
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) {
+        x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+        rem[s] = kIdleRem;
+        esc[s] = false;
+        dst[s] = p.out;
+    }
     unsigned long long my_iters = 0, my_pix = 0;
 
-    uint32_t trow = 0, jcur = 0, jend = 0;  // warp-uniform tile cursor
+    // warp-uniform tile cursor: columns [jcur, jend) of row trow
+    uint32_t jcur = 0, jend = 0;
+    T ci_tile = zero;            // Cy[trow] = ymax - trow*dy
+    uint32_t* row_ptr = p.out;   // &out[trow * W]
     bool more = true;
-    unsigned need = FULL;
+    unsigned need[ILP];
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) need[s] = FULL;
 
     for (;;) {
-        if (need) {
-            const uint32_t nd = __popc(need);
-            const uint32_t rank = __popc(need & lt_mask);
-            const bool mine = (need >> lane) & 1u;
+        // ---- refill: hand the next pixels of the tile stream to the free slots
+        uint32_t nd = 0, rank[ILP];
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            rank[s] = nd + __popc(need[s] & lt_mask);
+            nd += __popc(need[s]);
+        }
+        if (nd) {
             uint32_t served = 0;
-            while (served < nd) {
+            for (;;) {
                 if (jcur >= jend) {
                     if (!more) break;
                     int st = 0;
@@ -213,61 +251,263 @@ escape_refill_kernel(const Params p) {
                     st = __shfl_sync(FULL, st, 0);
                     if (st == kTileNone) { more = false; break; }
                     if (st == kTileSkip) continue;
-                    trow = __shfl_sync(FULL, r_, 0);
+                    const uint32_t trow = __shfl_sync(FULL, r_, 0);
                     jcur = __shfl_sync(FULL, a_, 0);
                     jend = __shfl_sync(FULL, b_, 0);
+                    ci_tile = A::sub(ymax, A::mul(A::cvt(trow), dy));  // Cy[i] = ymax - i*dy
+                    row_ptr = p.out + (size_t)trow * p.W;
                 }
                 const uint32_t take = min(jend - jcur, nd - served);
-                if (mine && rank >= served && rank < served + take) {
-                    const uint32_t j = jcur + (rank - served);
-                    cr = A::add(xmin, A::mul(A::cvt(j), dx));    // Cx[j] = xmin + j*dx
-                    ci = A::sub(ymax, A::mul(A::cvt(trow), dy)); // Cy[i] = ymax - i*dy
-                    x = y = x2 = y2 = zero;
-                    rem = p.iter_max;
-                    active = true;
-                    dst = p.out + ((size_t)trow * p.W + j);
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) {
+                    const uint32_t q = rank[s] - served;
+                    if (((need[s] >> lane) & 1u) && q < take) {
+                        const uint32_t j = jcur + q;
+                        cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
+                        ci[s] = ci_tile;
+                        x[s] = y[s] = x2[s] = y2[s] = zero;
+                        rem[s] = p.iter_max;
+                        dst[s] = row_ptr + j;
+                    }
                 }
                 jcur += take;
                 served += take;
+                if (served == nd) break;
+            }
+            if (served < nd) {
+                // the work is exhausted: unserved free slots go idle
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) {
+                    if (((need[s] >> lane) & 1u) && rank[s] >= served) {
+                        x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+                        rem[s] = kIdleRem;
+                    }
+                }
             }
         }
-        if (!__any_sync(FULL, active)) break;
+        uint32_t mrem = kIdleRem;
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) mrem = min(mrem, rem[s]);
+        const uint32_t kmax = __reduce_min_sync(FULL, mrem);
+        if (kmax == kIdleRem) break;  // every slot of the warp is idle: done
 
-        const uint32_t kmax = __reduce_min_sync(FULL, rem);
+        // ---- iterate: Eq. 1 on every slot until some slot is finished.  The hot loop
+        // tests a 32-bit candidate key (one compare per slot); on a candidate the warp
+        // leaves the loop and verifies the exact 64-bit test, resuming on a false alarm.
         uint32_t k = 0;
-        bool esc = false;
+        bool fin[ILP];
         for (;;) {
-            if (kmax - k >= 4) {
-                MANDEL_STEP();
-                if (__any_sync(FULL, esc)) { k += 1; break; }
-                MANDEL_STEP();
-                if (__any_sync(FULL, esc)) { k += 2; break; }
-                MANDEL_STEP();
-                if (__any_sync(FULL, esc)) { k += 3; break; }
-                MANDEL_STEP();
-                k += 4;
-                if (__any_sync(FULL, esc) || k == kmax) break;
-            } else {
-                MANDEL_STEP();
-                k += 1;
-                if (__any_sync(FULL, esc) || k == kmax) break;
+            for (;;) {
+                if (kmax - k >= 4) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        bool e = false;
+#pragma unroll
+                        for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
+#pragma unroll
+                        for (int s = 0; s < ILP; ++s) e |= esc[s];
+                        if (__any_sync(FULL, e)) { k += u + 1; goto left_loop; }
+                    }
+                    k += 4;
+                    if (k == kmax) break;
+                } else {
+                    bool e = false;
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) e |= esc[s];
+                    k += 1;
+                    if (__any_sync(FULL, e) || k == kmax) break;
+                }
             }
+        left_loop:
+            bool any_fin = false;
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) {
+                // exact Eq. 2 test on the candidate's own |z|^2 (same operands, same bits);
+                // idle slots hold z = 0 and never pass it
+                fin[s] = A::bits(A::add(x2[s], y2[s])) > r2;
+                any_fin |= fin[s];
+            }
+            if (k == kmax || __any_sync(FULL, any_fin)) break;
         }
-        bool done = false;
-        if (active) {
-            rem -= k;
-            done = esc || rem == 0;
+
+        // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            bool done = false;
+            if (rem[s] != kIdleRem) {
+                rem[s] -= k;
+                done = fin[s] || rem[s] == 0;
+            }
+            if (done) {
+                const uint32_t n = p.iter_max - rem[s];
+                *dst[s] = n;
+                my_iters += n;
+                my_pix += 1;
+            }
+            need[s] = __ballot_sync(FULL, done);
         }
-        if (done) {
-            const uint32_t n = p.iter_max - rem;
-            *dst = n;                     // a5 (+a6 when dst is rank 0's peer image)
-            my_iters += n;
-            my_pix += 1;
-            active = false;
-            x = y = x2 = y2 = cr = ci = zero;  // an idle lane iterates z = 0 forever
-            rem = kIdleRem;
+    }
+    flush_stats(p, my_iters, my_pix);
+}
+
+// ---------------------------------------------------------------------------
+// K1/K2 (lazy refill): like escape_refill_kernel, but a slot that escapes does
+// not end the inner loop.  Each slot keeps its own count n (incremented while
+// the slot is live) and a live flag cleared at its escape, so the exact escape
+// iteration is recorded in-loop; the warp leaves the loop only when at least
+// `refill_lanes` lanes hold a finished slot (then all finished slots are retired
+// and refilled at once), or when the earliest iterMax deadline is reached.  This
+// amortises the refill over several finished pixels -- the eager variant leaves
+// the loop on every escape, which dominates where neighbouring counts differ
+// (C4's zoom: one escape every ~4 warp-iterations).
+// Per slot per iteration: 8 FP ops + 2 compare + 1 count + 1 flag update.
+// ---------------------------------------------------------------------------
+// One z-update of slot s (lazy kernel): count it if the slot was live before it
+// (n counts the escaping update too, reading R3), then clear `lv` on escape.
+#define LAZY_STEP_SLOT(s)                                                  \
+    do {                                                                   \
+        T ny_ = A::add(A::mul(A::add(x[s], x[s]), y[s]), ci[s]);           \
+        T nx_ = A::add(A::sub(x2[s], y2[s]), cr[s]);                       \
+        x[s] = nx_;                                                        \
+        y[s] = ny_;                                                        \
+        x2[s] = A::mul(x[s], x[s]);                                        \
+        y2[s] = A::mul(y[s], y[s]);                                        \
+        const bool in_ = !(A::bits(A::add(x2[s], y2[s])) > r2);           \
+        n[s] += lv[s];                                                     \
+        lv[s] = in_ ? lv[s] : 0u;                                          \
+    } while (0)
+
+template <typename T, int ILP, bool DRAIN>
+__device__ __forceinline__ void lazy_run(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
+                                         const T (&cr)[ILP], const T (&ci)[ILP],
+                                         uint32_t (&n)[ILP], uint32_t (&lv)[ILP],
+                                         typename Arith<T>::bits_t r2, uint32_t kmax,
+                                         int max_live_full) {
+    typedef Arith<T> A;
+    const unsigned FULL = 0xffffffffu;
+    uint32_t k = 0;
+    for (;;) {
+        if (kmax - k >= 2) {
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
+            k += 2;
+        } else {
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
+            k += 1;
         }
-        need = __ballot_sync(FULL, done);
+        uint32_t acc = DRAIN ? 0u : 1u;
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) acc = DRAIN ? (acc | lv[s]) : (acc & lv[s]);
+        const int c = __popc(__ballot_sync(FULL, acc != 0u));
+        if (k == kmax || c <= max_live_full) break;
+    }
+}
+
+template <typename T, int ILP, int MINB>
+__global__ void __launch_bounds__(kCtaThreads, MINB)
+escape_lazy_kernel(const Params p) {
+    typedef Arith<T> A;
+    typedef typename A::bits_t B;
+    const unsigned FULL = 0xffffffffu;
+    const uint32_t lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const B r2 = (B)p.r2bits;
+    const T xmin = A::xmin(p), ymax = A::ymax(p), dx = A::dx(p), dy = A::dy(p);
+    const T zero = T(0);
+    const int max_live_full = 32 - (int)p.refill_lanes;  // exit when >= refill_lanes lanes have a free slot
+
+    T x[ILP], y[ILP], x2[ILP], y2[ILP], cr[ILP], ci[ILP];
+    uint32_t n[ILP];
+    uint32_t lv[ILP];  // 1 while the slot iterates (live), 0 after its escape or when idle
+    bool has[ILP];
+    uint32_t* dst[ILP];
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) {
+        x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+        n[s] = 0;
+        lv[s] = 0;
+        has[s] = false;
+        dst[s] = p.out;
+    }
+    unsigned long long my_iters = 0, my_pix = 0;
+    uint32_t trow = 0, jcur = 0, jend = 0;  // warp-uniform tile cursor
+    bool more = true;
+    unsigned need[ILP];
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) need[s] = FULL;
+
+    for (;;) {
+        // ---- refill free slots from the warp's tile stream
+        uint32_t nd = 0, rank[ILP];
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            rank[s] = nd + __popc(need[s] & lt_mask);
+            nd += __popc(need[s]);
+        }
+        uint32_t served = 0;
+        while (served < nd) {
+            if (jcur >= jend) {
+                if (!more) break;
+                int st = 0;
+                uint32_t r_ = 0, a_ = 0, b_ = 0;
+                if (lane == 0) st = draw_tile(p, r_, a_, b_);
+                st = __shfl_sync(FULL, st, 0);
+                if (st == kTileNone) { more = false; break; }
+                if (st == kTileSkip) continue;
+                trow = __shfl_sync(FULL, r_, 0);
+                jcur = __shfl_sync(FULL, a_, 0);
+                jend = __shfl_sync(FULL, b_, 0);
+            }
+            const uint32_t take = min(jend - jcur, nd - served);
+            const T ci_row = A::sub(ymax, A::mul(A::cvt(trow), dy));  // Cy[i] = ymax - i*dy
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) {
+                if (((need[s] >> lane) & 1u) && rank[s] >= served && rank[s] < served + take) {
+                    const uint32_t j = jcur + (rank[s] - served);
+                    cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
+                    ci[s] = ci_row;
+                    x[s] = y[s] = x2[s] = y2[s] = zero;
+                    n[s] = 0;
+                    lv[s] = 1;
+                    has[s] = true;
+                    dst[s] = p.out + ((size_t)trow * p.W + j);
+                }
+            }
+            jcur += take;
+            served += take;
+        }
+        // ---- iterate until enough slots are finished (or a deadline)
+        bool any_live = false;
+        uint32_t left = kIdleRem;
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            any_live |= lv[s] != 0;
+            if (lv[s]) left = min(left, p.iter_max - n[s]);
+        }
+        if (!__any_sync(FULL, any_live)) break;
+        const uint32_t kmax = __reduce_min_sync(FULL, left);
+        if (more) lazy_run<T, ILP, false>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, max_live_full);
+        else lazy_run<T, ILP, true>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, 0);
+
+        // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            const bool done = has[s] && (lv[s] == 0 || n[s] == p.iter_max);
+            if (done) {
+                *dst[s] = n[s];
+                my_iters += n[s];
+                my_pix += 1;
+                has[s] = false;
+                lv[s] = 0;
+                x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;  // idle: z = 0 forever
+            }
+            need[s] = __ballot_sync(FULL, done);
+        }
     }
     flush_stats(p, my_iters, my_pix);
 }
@@ -307,5 +547,7 @@ escape_static_kernel(const Params p) {
 }
 
 #undef MANDEL_STEP
+#undef MANDEL_STEP_SLOT
+#undef LAZY_STEP_SLOT
 
 }  // namespace mandel

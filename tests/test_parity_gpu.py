@@ -46,13 +46,18 @@ def _assert_same(got, want, label):
 # ---------------------------------------------------------------------------
 # whole maps: C1 and reduced shapes, every scheme, logical rank counts, kernels
 # ---------------------------------------------------------------------------
+KERNELS = ["refill", "refill1", "refill2", "refill3", "refill4", "lazy1", "lazy2"]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("dtype", ["fp64", "fp32"])
 @pytest.mark.parametrize("scheme", SCHEMES)
 @pytest.mark.parametrize("ngpus", [1, 2, 3, 5, 8])
-def test_c1_all_schemes(mandel, oracle, dtype, scheme, ngpus):
+def test_c1_all_schemes(mandel, oracle, dtype, scheme, ngpus, kernel):
     cfg = wl.C1.with_(dtype=dtype)
     want = oracle.render(cfg)
-    out, st = _render_dev(mandel, cfg, scheme, ngpus)
+    out, st = _render_dev(mandel, cfg, scheme, ngpus, kernel=kernel,
+                          refill_lanes=[0, 1, 5, 32][ngpus % 4])
     _assert_same(_host(out), want, f"C1/{dtype}/{scheme}/N={ngpus}")
     assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
     assert st["pixels"] == cfg.pixels
@@ -73,8 +78,9 @@ def test_static_kernel_variant(mandel, oracle, dtype, scheme):
     _assert_same(_host(out), oracle.render(cfg), f"static/{dtype}/{scheme}")
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("dtype", ["fp64", "fp32"])
-def test_random_small_configs(mandel, oracle, dtype):
+def test_random_small_configs(mandel, oracle, dtype, kernel):
     for k, cfg in enumerate(wl.random_small_configs(50, 0, dtype)):
         want = oracle.render(cfg)
         scheme = SCHEMES[k % 3]
@@ -82,7 +88,8 @@ def test_random_small_configs(mandel, oracle, dtype):
         if scheme != "fcfs" and cfg.H < ngpus:
             ngpus = 1
         out, st = _render_dev(mandel, cfg, scheme, ngpus, tile_px=[0, 1, 7, 32, 33][k % 5],
-                              chunk_rows=[0, 1, 3][k % 3])
+                              chunk_rows=[0, 1, 3][k % 3], kernel=kernel,
+                              refill_lanes=[0, 1, 3, 16, 32][k % 5])
         _assert_same(_host(out), want, f"{cfg.name}/{dtype}/{scheme}/N={ngpus}")
         assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
 
@@ -101,14 +108,15 @@ EDGE = [
 ]
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("cfg", EDGE, ids=[c.name for c in EDGE])
 @pytest.mark.parametrize("scheme", SCHEMES)
-def test_edge_cases(mandel, oracle, cfg, scheme):
+def test_edge_cases(mandel, oracle, cfg, scheme, kernel):
     want = oracle.render(cfg)
     for ngpus in (1, 4):
         if scheme != "fcfs" and cfg.H < ngpus:
             continue
-        out, st = _render_dev(mandel, cfg, scheme, ngpus)
+        out, st = _render_dev(mandel, cfg, scheme, ngpus, kernel=kernel)
         got = _host(out)
         _assert_same(got, want, f"{cfg.name}/{scheme}/N={ngpus}")
         assert got.min() >= 1 and got.max() <= cfg.iter_max
@@ -159,10 +167,11 @@ def _properties(oracle, cfg, out, st):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("kernel", ["refill", "lazy2"])
 @pytest.mark.parametrize("name,nrows", [("C2", 48), ("C3", 48), ("C4", 16)])
-def test_full_size_sampled(mandel, oracle, name, nrows):
+def test_full_size_sampled(mandel, oracle, name, nrows, kernel):
     cfg = wl.CONFIGS[name]
-    out, st = _render_dev(mandel, cfg, "fcfs", 1)
+    out, st = _render_dev(mandel, cfg, "fcfs", 1, kernel=kernel)
     _properties(oracle, cfg, out, st)
     _sampled_rows_check(oracle, cfg, out, nrows, seed=sum(map(ord, name)))
     if name in ("C2", "C3"):

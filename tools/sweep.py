@@ -1,0 +1,86 @@
+#!/usr/bin/env python3
+"""Kernel-variant sweep on one GPU (development tool, not the bench).
+
+    python tools/sweep.py --configs C2,C4 --kernels refill1,refill2,static \
+        --schemes block,fcfs --tiles 256,512 --steps 10
+
+Every variant's map is compared with the first variant's map on the device
+(all variants must be bit-identical; parity with the oracle is the tests' job).
+Prints one JSON line per variant.
+"""
+import argparse
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import workloads as wl  # noqa: E402
+from paper_2007_00745_b200 import mandel  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C2")
+    ap.add_argument("--kernels", default="refill1,refill2")
+    ap.add_argument("--schemes", default="block,fcfs")
+    ap.add_argument("--tiles", default="256")
+    ap.add_argument("--chunks", default="16")
+    ap.add_argument("--lanes", default="8")
+    ap.add_argument("--minb", default="1")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=2)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    for name in a.configs.split(","):
+        cfg = wl.CONFIGS[name]
+        ref = None
+        out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
+        for kern, scheme, tile, chunk, lanes, minb in itertools.product(
+                a.kernels.split(","), a.schemes.split(","), a.tiles.split(","), a.chunks.split(","),
+                a.lanes.split(","), a.minb.split(",")):
+            if kern == "static" and scheme == "fcfs":
+                continue
+            if not kern.startswith("lazy") and lanes != a.lanes.split(",")[0]:
+                continue
+            if kern == "static" and minb != a.minb.split(",")[0]:
+                continue
+            kw = dict(out_dev0=out, stream0=stream.cuda_stream, kernel=kern,
+                      tile_px=int(tile), chunk_rows=int(chunk), refill_lanes=int(lanes),
+                      min_ctas=int(minb) if kern != "static" else 0)
+            out.zero_()
+            for _ in range(a.warmup):
+                mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, 1, **kw)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ks = []
+            for _ in range(a.steps):
+                st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, 1, **kw)
+                ks.append(st["kernel_ms_max"])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.steps
+            if ref is None:
+                ref = out.clone()
+                same = True
+            else:
+                same = bool((ref == out).all())
+            giter = st["sum_iters"] / (ms * 1e-3) / 1e9
+            peak = 148 * (64 if cfg.dtype == "fp64" else 128) * 1.965e9 / 8 / 1e9
+            print(json.dumps({"config": name, "kernel": kern, "scheme": scheme, "tile": int(tile),
+                              "chunk": int(chunk), "lanes": int(lanes), "minb": int(minb), "ms": round(ms, 4),
+                              "kernel_ms": round(sum(ks) / len(ks), 4),
+                              "giter_s": round(giter, 2), "frac": round(giter / peak, 4),
+                              "identical": same}), flush=True)
+        del out, ref
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
