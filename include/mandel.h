@@ -76,8 +76,10 @@ enum mandel_kernel {
     MANDEL_KERNEL_REFILL = 0,  /* default: the fastest measured configuration for the dtype      */
     MANDEL_KERNEL_STATIC = 1,  /* one pixel per thread, static grid (baseline; BLOCK/CYCLIC only)  */
     MANDEL_KERNEL_EAGER = 2,   /* persistent CTAs, warp tile queue, lane refill on every escape   */
-    MANDEL_KERNEL_LAZY = 3     /* the same, refill batched: escapes recorded in-loop, the warp
+    MANDEL_KERNEL_LAZY = 3,    /* the same, refill batched: escapes recorded in-loop, the warp
                                   refills when refill_lanes lanes hold a finished pixel          */
+    MANDEL_KERNEL_ADAPTIVE = 4 /* per warp and run: EAGER while escapes are sparse, LAZY while
+                                  they are dense (runs shorter than adapt_lo iterations)         */
 };
 
 /* Per-call statistics (all fields written when stats != NULL and the call succeeds). */
@@ -109,9 +111,10 @@ typedef struct mandel_options {
                                 g % count on its own stream (tests; ranks never wait on each other) */
     int      refill_lanes;   /* LAZY: lanes with a finished pixel that trigger a refill (1..32);
                                 0 -> library default                                               */
-    int      ilp;            /* EAGER/LAZY: pixels per lane (EAGER 1..4, LAZY 1..2); 0 -> default  */
-    int      min_ctas;       /* EAGER/LAZY: register budget as CTAs per SM (1,4,5,6,8); 0 -> default */
-    int      reserved;
+    int      ilp;            /* pixels per lane (EAGER 1..4, LAZY/ADAPTIVE 1..2); 0 -> default     */
+    int      min_ctas;       /* register budget as CTAs per SM (1,4,5,6,8); 0 -> default           */
+    int      adapt_lo;       /* ADAPTIVE: eager->lazy below this run length; 0 -> default          */
+    int      adapt_hi;       /* ADAPTIVE: lazy->eager above this run length; 0 -> default          */
 } mandel_options;
 
 /*

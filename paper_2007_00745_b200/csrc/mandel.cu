@@ -139,7 +139,7 @@ int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
 struct DeviceCtx {
     bool init = false;
     int sms = 0;
-    int occ_cache[2][4][5][5] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
+    int occ_cache[2][5][5][5] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
     bool peer_to0 = false;
 };
 
@@ -196,10 +196,15 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
         {MANDEL_MINB_ROW(escape_lazy_kernel, double, 1), MANDEL_MINB_ROW(escape_lazy_kernel, double, 2)},
         {MANDEL_MINB_ROW(escape_lazy_kernel, float, 1), MANDEL_MINB_ROW(escape_lazy_kernel, float, 2)},
     };
+    static const KernelFn adaptive[2][2][5] = {
+        {MANDEL_MINB_ROW(escape_adaptive_kernel, double, 1), MANDEL_MINB_ROW(escape_adaptive_kernel, double, 2)},
+        {MANDEL_MINB_ROW(escape_adaptive_kernel, float, 1), MANDEL_MINB_ROW(escape_adaptive_kernel, float, 2)},
+    };
     if (variant == MANDEL_KERNEL_STATIC) return fp32 ? escape_static_kernel<float> : escape_static_kernel<double>;
     if (mi < 0 || mi > 4) return nullptr;
     if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
     if (variant == MANDEL_KERNEL_LAZY && ilp >= 1 && ilp <= 2) return lazy[fp32][ilp - 1][mi];
+    if (variant == MANDEL_KERNEL_ADAPTIVE && ilp >= 1 && ilp <= 2) return adaptive[fp32][ilp - 1][mi];
     return nullptr;
 }
 
@@ -210,6 +215,7 @@ struct KernelChoice {
 constexpr KernelChoice kDefaultChoice[2] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp64: C2 75.6%, C5 84.4%
                                             {MANDEL_KERNEL_EAGER, 4, 1}};  // fp32: C3 53.8% (issue-bound)
 constexpr uint32_t kDefaultRefillLanes = 8;
+constexpr uint32_t kDefaultAdaptLo = 16, kDefaultAdaptHi = 64;
 
 int device_count(int& n) {
     n = 0;
@@ -261,7 +267,9 @@ int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
         rc.device = dev;
     }
     CK(cudaSetDevice(dev));
-    if (!rc.stream) CK(cudaStreamCreateWithFlags(&rc.stream, cudaStreamNonBlocking));
+    // blocking streams: ordered after work the caller queued on the legacy default stream
+    // (e.g. torch.zeros of the destination) when no stream0 is passed
+    if (!rc.stream) CK(cudaStreamCreateWithFlags(&rc.stream, cudaStreamDefault));
     if (!rc.k0) CK(cudaEventCreate(&rc.k0));
     if (!rc.k1) CK(cudaEventCreate(&rc.k1));
     if (rc.state_bytes < state_bytes) {
@@ -302,7 +310,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     int rc = make_plan(scheme, H, nranks, rank, pl);
     if (rc) return rc;
     const int kernel = o ? o->kernel : MANDEL_KERNEL_REFILL;
-    if (kernel < MANDEL_KERNEL_REFILL || kernel > MANDEL_KERNEL_LAZY)
+    if (kernel < MANDEL_KERNEL_REFILL || kernel > MANDEL_KERNEL_ADAPTIVE)
         return fail(MANDEL_EINVAL, "options.kernel out of range");
     if (kernel == MANDEL_KERNEL_STATIC && scheme == MANDEL_FCFS)
         return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
@@ -352,6 +360,8 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;
     if (rl < 1 || rl > 32) return fail(MANDEL_EINVAL, "options.refill_lanes must be in 1..32");
     p.refill_lanes = (uint32_t)rl;
+    p.adapt_lo = (o && o->adapt_lo > 0) ? (uint32_t)o->adapt_lo : kDefaultAdaptLo;
+    p.adapt_hi = (o && o->adapt_hi > 0) ? (uint32_t)o->adapt_hi : kDefaultAdaptHi;
     ls.block = persistent ? dim3(mandel::kCtaThreads) : dim3(32, mandel::kWarpsPerCta);
     if (persistent) {
         int occ = 1;

@@ -51,6 +51,8 @@ struct Params {
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
     uint32_t refill_lanes;           // lazy refill: leave the loop when this many lanes are free
+    uint32_t adapt_lo, adapt_hi;     // adaptive: eager->lazy below adapt_lo iterations per run,
+                                     // lazy->eager above adapt_hi
     uint32_t* out;                   // rank 0's image, row-major W per row (local or peer)
     WorkState* ws;                   // this rank's state (local memory)
     uint32_t* chunk_map;             // this rank's local->global chunk table (local memory)
@@ -511,6 +513,211 @@ escape_lazy_kernel(const Params p) {
     }
     flush_stats(p, my_iters, my_pix);
 }
+
+// ---------------------------------------------------------------------------
+// K1/K2 (adaptive): the eager kernel's state and exits, plus the lazy kernel's
+// in-loop escape bookkeeping, chosen per warp and per run.  A warp whose eager
+// runs end after fewer than adapt_lo iterations (escapes are dense and
+// incoherent, e.g. C4's zoom) switches to lazy runs, which retire and refill
+// only when refill_lanes lanes hold a finished pixel; a lazy run longer than
+// adapt_hi switches back to eager runs (sparse, coherent escapes: C2, C5).
+// Lazy per-slot bookkeeping: `rem -= lv` and `lv = in ? lv : 0` every iteration
+// with the exact 64-bit Eq. 2 test (rem = iterations still allowed; lv = live).
+// ---------------------------------------------------------------------------
+#define ADAPT_LAZY_STEP_SLOT(s)                                            \
+    do {                                                                   \
+        T ny_ = A::add(A::mul(A::add(x[s], x[s]), y[s]), ci[s]);           \
+        T nx_ = A::add(A::sub(x2[s], y2[s]), cr[s]);                       \
+        x[s] = nx_;                                                        \
+        y[s] = ny_;                                                        \
+        x2[s] = A::mul(x[s], x[s]);                                        \
+        y2[s] = A::mul(y[s], y[s]);                                        \
+        const bool in_ = !(A::bits(A::add(x2[s], y2[s])) > r2);           \
+        rem[s] -= lv[s];                                                   \
+        lv[s] = in_ ? lv[s] : 0u;                                          \
+    } while (0)
+
+template <typename T, int ILP, int MINB>
+__global__ void __launch_bounds__(kCtaThreads, MINB)
+escape_adaptive_kernel(const Params p) {
+    typedef Arith<T> A;
+    typedef typename A::bits_t B;
+    const unsigned FULL = 0xffffffffu;
+    const uint32_t lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const B r2 = (B)p.r2bits;
+    const int r2c = p.r2cand;
+    const T xmin = A::xmin(p), ymax = A::ymax(p), dx = A::dx(p), dy = A::dy(p);
+    const T zero = T(0);
+    const int max_live_full = 32 - (int)p.refill_lanes;
+
+    T x[ILP], y[ILP], x2[ILP], y2[ILP], cr[ILP], ci[ILP];
+    uint32_t rem[ILP];
+    bool esc[ILP];
+    uint32_t* dst[ILP];
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) {
+        x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+        rem[s] = kIdleRem;
+        esc[s] = false;
+        dst[s] = p.out;
+    }
+    unsigned long long my_iters = 0, my_pix = 0;
+    uint32_t jcur = 0, jend = 0;
+    T ci_tile = zero;
+    uint32_t* row_ptr = p.out;
+    bool more = true;
+    bool lazy = false;  // warp-uniform run mode
+    unsigned need[ILP];
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) need[s] = FULL;
+
+    for (;;) {
+        // ---- refill (as escape_refill_kernel)
+        uint32_t nd = 0, rank[ILP];
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            rank[s] = nd + __popc(need[s] & lt_mask);
+            nd += __popc(need[s]);
+        }
+        if (nd) {
+            uint32_t served = 0;
+            for (;;) {
+                if (jcur >= jend) {
+                    if (!more) break;
+                    int st = 0;
+                    uint32_t r_ = 0, a_ = 0, b_ = 0;
+                    if (lane == 0) st = draw_tile(p, r_, a_, b_);
+                    st = __shfl_sync(FULL, st, 0);
+                    if (st == kTileNone) { more = false; break; }
+                    if (st == kTileSkip) continue;
+                    const uint32_t trow = __shfl_sync(FULL, r_, 0);
+                    jcur = __shfl_sync(FULL, a_, 0);
+                    jend = __shfl_sync(FULL, b_, 0);
+                    ci_tile = A::sub(ymax, A::mul(A::cvt(trow), dy));  // Cy[i] = ymax - i*dy
+                    row_ptr = p.out + (size_t)trow * p.W;
+                }
+                const uint32_t take = min(jend - jcur, nd - served);
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) {
+                    const uint32_t q = rank[s] - served;
+                    if (((need[s] >> lane) & 1u) && q < take) {
+                        const uint32_t j = jcur + q;
+                        cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
+                        ci[s] = ci_tile;
+                        x[s] = y[s] = x2[s] = y2[s] = zero;
+                        rem[s] = p.iter_max;
+                        dst[s] = row_ptr + j;
+                    }
+                }
+                jcur += take;
+                served += take;
+                if (served == nd) break;
+            }
+            if (served < nd) {
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) {
+                    if (((need[s] >> lane) & 1u) && rank[s] >= served) {
+                        x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+                        rem[s] = kIdleRem;
+                    }
+                }
+            }
+        }
+        uint32_t mrem = kIdleRem;
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) mrem = min(mrem, rem[s]);
+        const uint32_t kmax = __reduce_min_sync(FULL, mrem);
+        if (kmax == kIdleRem) break;
+
+        uint32_t k = 0;
+        bool fin[ILP];
+        if (!lazy) {
+            // ---- eager run (candidate key, exact verification; see escape_refill_kernel)
+            for (;;) {
+                for (;;) {
+                    if (kmax - k >= 4) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            bool e = false;
+#pragma unroll
+                            for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
+#pragma unroll
+                            for (int s = 0; s < ILP; ++s) e |= esc[s];
+                            if (__any_sync(FULL, e)) { k += u + 1; goto eager_left; }
+                        }
+                        k += 4;
+                        if (k == kmax) break;
+                    } else {
+                        bool e = false;
+#pragma unroll
+                        for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
+#pragma unroll
+                        for (int s = 0; s < ILP; ++s) e |= esc[s];
+                        k += 1;
+                        if (__any_sync(FULL, e) || k == kmax) break;
+                    }
+                }
+            eager_left:
+                bool any_fin = false;
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) {
+                    fin[s] = A::bits(A::add(x2[s], y2[s])) > r2;
+                    any_fin |= fin[s];
+                }
+                if (k == kmax || __any_sync(FULL, any_fin)) break;
+            }
+#pragma unroll
+            for (int s = 0; s < ILP; ++s)
+                if (rem[s] != kIdleRem) rem[s] -= k;
+            if (k < p.adapt_lo) lazy = true;
+        } else {
+            // ---- lazy run: per-slot exact bookkeeping, leave when enough lanes are free
+            uint32_t lv[ILP];
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) lv[s] = rem[s] != kIdleRem ? 1u : 0u;
+            const int thr = more ? max_live_full : 0;
+            for (;;) {
+                if (kmax - k >= 2) {
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) ADAPT_LAZY_STEP_SLOT(s);
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) ADAPT_LAZY_STEP_SLOT(s);
+                    k += 2;
+                } else {
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) ADAPT_LAZY_STEP_SLOT(s);
+                    k += 1;
+                }
+                uint32_t acc = more ? 1u : 0u;
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) acc = more ? (acc & lv[s]) : (acc | lv[s]);
+                const int c = __popc(__ballot_sync(FULL, acc != 0u));
+                if (k == kmax || c <= thr) break;
+            }
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) fin[s] = lv[s] == 0u;  // escaped (or idle)
+            if (k > p.adapt_hi) lazy = false;
+        }
+
+        // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            bool done = false;
+            if (rem[s] != kIdleRem) done = fin[s] || rem[s] == 0;
+            if (done) {
+                const uint32_t n = p.iter_max - rem[s];
+                *dst[s] = n;
+                my_iters += n;
+                my_pix += 1;
+            }
+            need[s] = __ballot_sync(FULL, done);
+        }
+    }
+    flush_stats(p, my_iters, my_pix);
+}
+
+#undef ADAPT_LAZY_STEP_SLOT
 
 // ---------------------------------------------------------------------------
 // Baseline variant: one pixel per thread over a static 2D grid (32 x 8 threads,

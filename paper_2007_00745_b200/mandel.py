@@ -23,10 +23,12 @@ MANDEL_BLOCK, MANDEL_CYCLIC, MANDEL_FCFS = 0, 1, 2
 MANDEL_OK, MANDEL_EINVAL, MANDEL_ENODEV, MANDEL_ENOMEM = 0, -1, -2, -3
 MANDEL_ECUDA, MANDEL_ECOMM, MANDEL_EBUSY = -4, -5, -6
 MANDEL_KERNEL_REFILL, MANDEL_KERNEL_STATIC, MANDEL_KERNEL_EAGER, MANDEL_KERNEL_LAZY = 0, 1, 2, 3
+MANDEL_KERNEL_ADAPTIVE = 4
 # name -> (mandel_kernel, ilp); ilp 0 = the library's default for that kernel
 KERNELS = {"refill": (0, 0), "static": (1, 0), "eager": (2, 0), "lazy": (3, 0),
            "refill1": (2, 1), "refill2": (2, 2), "refill3": (2, 3), "refill4": (2, 4),
-           "lazy1": (3, 1), "lazy2": (3, 2)}
+           "lazy1": (3, 1), "lazy2": (3, 2), "adaptive": (4, 0), "adaptive1": (4, 1),
+           "adaptive2": (4, 2)}
 MANDEL_MAX_GPUS = 64
 MANDEL_IPC_HANDLE_BYTES = 64
 
@@ -84,7 +86,8 @@ class mandel_options(ctypes.Structure):
         ("refill_lanes", ctypes.c_int),
         ("ilp", ctypes.c_int),
         ("min_ctas", ctypes.c_int),
-        ("reserved", ctypes.c_int),
+        ("adapt_lo", ctypes.c_int),
+        ("adapt_hi", ctypes.c_int),
     ]
 
 
@@ -174,7 +177,7 @@ def _ptr(a) -> int | None:
 
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
-          refill_lanes=0, ilp=0, min_ctas=0):
+          refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -183,6 +186,8 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.refill_lanes = refill_lanes or 0
     o.ilp = ilp or 0
     o.min_ctas = min_ctas or 0
+    o.adapt_lo = adapt_lo or 0
+    o.adapt_hi = adapt_hi or 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -212,12 +217,13 @@ def mandel_render(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, ngpu
 def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", scheme="block",
                      ngpus=1, *, out_host=None, out_dev0=None, stream0=None, chunk_rows=0,
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
-                     refill_lanes=0, ilp=0, min_ctas=0) -> dict:
+                     refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0) -> dict:
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict."""
     st = mandel_stats()
-    o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas)
+    o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
+              adapt_hi)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st))
@@ -228,11 +234,11 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
 def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, rank, nranks,
                        out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
                        kernel=MANDEL_KERNEL_REFILL, refill_lanes=0, ilp=0,
-                       min_ctas=0) -> dict:
+                       min_ctas=0, adapt_lo=0, adapt_hi=0) -> dict:
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
     pointers valid in this process (own, or mapped with mandel_ipc_open)."""
     st = mandel_stats()
-    o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas)
+    o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas, adapt_lo, adapt_hi)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
                                   _ptr(out_root), _ptr(fcfs_counter), stream, ctypes.byref(st))

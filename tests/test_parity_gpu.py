@@ -26,6 +26,10 @@ def _torch():
 def _render_dev(mandel, cfg, scheme="block", ngpus=1, **kw):
     torch = _torch()
     out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device="cuda:0")
+    # every other call leaves stream0 unset: the library's own (blocking) stream must then
+    # still be ordered after torch's zero-fill on the default stream
+    if kw.pop("pass_stream", True) and (cfg.W + cfg.H) % 2 == 0:
+        kw["stream0"] = torch.cuda.current_stream().cuda_stream
     st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, ngpus, out_dev0=out,
                                  logical_ranks=ngpus > 1, **kw)
     return out, st
@@ -46,7 +50,7 @@ def _assert_same(got, want, label):
 # ---------------------------------------------------------------------------
 # whole maps: C1 and reduced shapes, every scheme, logical rank counts, kernels
 # ---------------------------------------------------------------------------
-KERNELS = ["refill", "refill1", "refill2", "refill3", "refill4", "lazy1", "lazy2"]
+KERNELS = ["refill", "refill1", "refill2", "refill3", "refill4", "lazy1", "lazy2", "adaptive1", "adaptive2"]
 
 
 @pytest.mark.parametrize("kernel", KERNELS)

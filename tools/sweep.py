@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--chunks", default="16")
     ap.add_argument("--lanes", default="8")
     ap.add_argument("--minb", default="1")
+    ap.add_argument("--adapt", default="16:64", help="lo:hi pairs, comma separated")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=2)
     a = ap.parse_args()
@@ -41,18 +42,21 @@ def main():
         cfg = wl.CONFIGS[name]
         ref = None
         out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
-        for kern, scheme, tile, chunk, lanes, minb in itertools.product(
+        for kern, scheme, tile, chunk, lanes, minb, adapt in itertools.product(
                 a.kernels.split(","), a.schemes.split(","), a.tiles.split(","), a.chunks.split(","),
-                a.lanes.split(","), a.minb.split(",")):
+                a.lanes.split(","), a.minb.split(","), a.adapt.split(",")):
+            if not kern.startswith("adaptive") and adapt != a.adapt.split(",")[0]:
+                continue
+            alo, ahi = (int(v) for v in adapt.split(":"))
             if kern == "static" and scheme == "fcfs":
                 continue
-            if not kern.startswith("lazy") and lanes != a.lanes.split(",")[0]:
+            if not kern.startswith(("lazy", "adaptive")) and lanes != a.lanes.split(",")[0]:
                 continue
             if kern == "static" and minb != a.minb.split(",")[0]:
                 continue
             kw = dict(out_dev0=out, stream0=stream.cuda_stream, kernel=kern,
                       tile_px=int(tile), chunk_rows=int(chunk), refill_lanes=int(lanes),
-                      min_ctas=int(minb) if kern != "static" else 0)
+                      min_ctas=int(minb) if kern != "static" else 0, adapt_lo=alo, adapt_hi=ahi)
             out.zero_()
             for _ in range(a.warmup):
                 mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, 1, **kw)
@@ -74,7 +78,7 @@ def main():
             giter = st["sum_iters"] / (ms * 1e-3) / 1e9
             peak = 148 * (64 if cfg.dtype == "fp64" else 128) * 1.965e9 / 8 / 1e9
             print(json.dumps({"config": name, "kernel": kern, "scheme": scheme, "tile": int(tile),
-                              "chunk": int(chunk), "lanes": int(lanes), "minb": int(minb), "ms": round(ms, 4),
+                              "chunk": int(chunk), "lanes": int(lanes), "minb": int(minb), "adapt": adapt, "ms": round(ms, 4),
                               "kernel_ms": round(sum(ks) / len(ks), 4),
                               "giter_s": round(giter, 2), "frac": round(giter / peak, 4),
                               "identical": same}), flush=True)
