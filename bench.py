@@ -60,7 +60,8 @@ def parse():
     ap.add_argument("--config", default="C2", choices=sorted(wl.CONFIGS))
     ap.add_argument("--scheme", default="fcfs", choices=["block", "cyclic", "fcfs"])
     ap.add_argument("--chunk-rows", type=int, default=16)
-    ap.add_argument("--kernel", choices=["refill", "static"], default="refill")
+    ap.add_argument("--kernel", default="refill",
+                    help="refill (default), static, eager, lazy, adaptive, refill1..4, lazy1/2")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="target CPU work (core-seconds) of the cpu_baseline sample")
@@ -148,22 +149,8 @@ def dist_env():
 
 
 def aggregate(dist, rank_ms: float, rank_iters: int, device=None):
-    """Whole-job numbers: max over ranks of the timed region, sum of iterations."""
-    if dist is None:
-        return rank_ms, rank_iters
-    import torch
-    t = torch.tensor([rank_ms], dtype=torch.float64, device=device)
-    n = torch.tensor([rank_iters], dtype=torch.int64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dist.all_reduce(n, op=dist.ReduceOp.SUM)
-    return float(t.item()), int(n.item())
-
-
-def share_handles(dist, rank: int, handles):
-    """Broadcast rank 0's IPC handles (bytes) to every rank."""
-    obj = [handles if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
-    return obj[0]
+    from paper_2007_00745_b200.multiproc import aggregate as _agg
+    return _agg(dist, rank_ms, rank_iters, device)
 
 
 # ---------------------------------------------------------------------------
@@ -187,45 +174,31 @@ def run_ours(args):
         dist_mod.init_process_group("nccl", device_id=dev)
         dist = dist_mod
     mandel.lib()
-    kernel = mandel.MANDEL_KERNEL_STATIC if args.kernel == "static" else mandel.MANDEL_KERNEL_REFILL
+    if args.kernel not in mandel.KERNELS:
+        raise SystemExit(f"unknown --kernel {args.kernel}; choose from {sorted(mandel.KERNELS)}")
+    kernel = args.kernel
     stream = torch.cuda.current_stream(dev)
     s_handle = stream.cuda_stream
     nbytes = cfg.W * cfg.H * 4
 
     # the root image (rank 0) and the shared FCFS counter, IPC-mapped on the other ranks
-    own = []
+    rr = None
     if world == 1:
         img = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
         img_ptr = img.data_ptr()
-        ctr_ptr = None
     else:
-        if rank == 0:
-            img_ptr = mandel.mandel_dev_alloc(local, nbytes)
-            ctr_ptr = mandel.mandel_dev_alloc(local, 256)
-            own = [img_ptr, ctr_ptr]
-            hs = share_handles(dist, rank, (mandel.mandel_ipc_handle(img_ptr),
-                                            mandel.mandel_ipc_handle(ctr_ptr)))
-        else:
-            hs = share_handles(dist, rank, None)
-            img_ptr = mandel.mandel_ipc_open(hs[0])
-            ctr_ptr = mandel.mandel_ipc_open(hs[1])
-        dist.barrier()
+        from paper_2007_00745_b200.multiproc import RankRenderer
+        rr = RankRenderer(dist, rank, world, local, cfg.args(), cfg.dtype, s_handle)
+        img_ptr = rr.img
+        img = None
 
     def step(scheme, out_host=None):
         if world == 1:
             return mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, 1,
-                                           out_host=out_host,
-                                           out_dev0=img_ptr if out_host is None else img_ptr,
+                                           out_host=out_host, out_dev0=img_ptr,
                                            stream0=s_handle, chunk_rows=args.chunk_rows,
                                            kernel=kernel)
-        # multi-process: reset the shared counter, line up, render this rank's rows
-        if scheme == "fcfs" and rank == 0:
-            mandel.mandel_dev_zero(ctr_ptr, 256, s_handle)
-        dist.barrier()
-        st = mandel.mandel_render_rank(*cfg.args(), cfg.dtype, scheme, rank, world, img_ptr,
-                                       ctr_ptr, s_handle, chunk_rows=args.chunk_rows,
-                                       kernel=kernel)
-        dist.barrier()
+        st = rr.step(scheme, chunk_rows=args.chunk_rows, kernel=kernel)
         if out_host is not None and rank == 0:
             _d2h(out_host, img_ptr, nbytes, s_handle)  # rank 0 holds the whole map
         return st
@@ -343,13 +316,7 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()
-        if rank != 0:
-            mandel.mandel_ipc_close(img_ptr)
-            mandel.mandel_ipc_close(ctr_ptr)
-        dist.barrier()
-        for p in own:
-            mandel.mandel_dev_free(p)
+        rr.close()
         dist.destroy_process_group()
 
 

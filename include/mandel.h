@@ -167,7 +167,8 @@ int mandel_render_ex(double xmin, double xmax, double ymin, double ymax,
  *                  memory, IPC-mapped elsewhere); must be 0 before any rank starts and is
  *                  only used by MANDEL_FCFS (may be NULL otherwise).  The caller resets it
  *                  and separates renders with a barrier.
- *   stream       : nullable cudaStream_t of the current device.
+ *   stream       : nullable cudaStream_t; the rank runs on the stream's device (else on the
+ *                  calling thread's current device).
  * The call returns when this rank's rows are stored in the root image.  stats (nullable)
  * receives this rank's kernel_ms / rank_iters[0] / rank_pixels[0] / chunks_claimed.
  * Errors: as mandel_render_ex, plus EINVAL for rank outside [0, nranks) or a NULL out_root,
@@ -184,14 +185,14 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax,
  * Device memory shared across processes (CUDA IPC).  mandel_dev_alloc returns a
  * cudaMalloc'd block on `device` (so IPC handles address it at offset 0);
  * mandel_ipc_handle writes MANDEL_IPC_HANDLE_BYTES bytes describing it;
- * mandel_ipc_open maps another process's block into this process (on the current
- * device, peer access enabled lazily); mandel_ipc_close unmaps it.
+ * mandel_ipc_open maps another process's block into this process for use on `device`
+ * (peer access enabled lazily); mandel_ipc_close unmaps it.
  * Errors: EINVAL on NULL arguments, ENOMEM, ECOMM when the IPC call fails.
  */
 int mandel_dev_alloc(int device, size_t bytes, void **dev_ptr);
 int mandel_dev_free(void *dev_ptr);
 int mandel_ipc_handle(void *dev_ptr, void *handle_out);
-int mandel_ipc_open(const void *handle, void **dev_ptr_out);
+int mandel_ipc_open(int device, const void *handle, void **dev_ptr_out);
 int mandel_ipc_close(void *dev_ptr);
 /* Zero `bytes` bytes at dev_ptr (any device pointer valid in this process) on `stream`
  * (nullable = the legacy default stream of the current device) and wait for it.

@@ -305,7 +305,7 @@ int occupancy(int device, int fp32, int variant, int ilp, int mi, KernelFn fn, i
 
 int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
-                 uint32_t* fcfs_ctr, int device, LaunchSpec& ls) {
+                 uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls) {
     Plan pl;
     int rc = make_plan(scheme, H, nranks, rank, pl);
     if (rc) return rc;
@@ -342,6 +342,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.ws = reinterpret_cast<mandel::WorkState*>(state);
     p.chunk_map = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(state) + sizeof(mandel::WorkState));
     p.fcfs_ctr = fcfs_ctr;
+    p.fcfs_sys = fcfs_sys ? 1u : 0u;
     const DeviceCtx& dc = g_dev[device];
     const int fi = dtype == MANDEL_FP32 ? 1 : 0;
     KernelChoice kc = kDefaultChoice[fi];
@@ -444,7 +445,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         rc = ensure_rank(r, dev, sbytes, nullptr);
         if (rc) return rc;
         rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, g_rank[r].state,
-                          g_root.fcfs_ctr, dev, specs[r]);
+                          g_root.fcfs_ctr, nphys > 1, dev, specs[r]);
         if (rc) return rc;
     }
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
@@ -618,8 +619,11 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     int ndev = 0;
     rc = device_count(ndev);
     if (rc) return rc;
+    // the device this rank runs on: the caller's stream's device, else the current device
     int dev = 0;
-    CK(cudaGetDevice(&dev));
+    if (streamv) CK(cudaStreamGetDevice((cudaStream_t)streamv, &dev));
+    else CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= ndev) return fail(MANDEL_ENODEV, "stream device out of range");
     rc = ensure_device(dev);
     if (rc) return rc;
     const size_t sbytes = state_bytes_for(H, opts);
@@ -628,8 +632,9 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     if (rc) return rc;
     RankCtx& rk = g_rank[0];
     LaunchSpec ls;
+    // across processes the counter is (in general) on another GPU: system scope
     rc = build_params(d, W, H, iterMax, dtype, scheme, nranks, rank, opts, out_root, rk.state,
-                      fcfs_counter, dev, ls);
+                      fcfs_counter, nranks > 1, dev, ls);
     if (rc) return rc;
     cudaStream_t s = streamv ? (cudaStream_t)streamv : rk.stream;
     const double t0 = now_ms();
@@ -690,10 +695,11 @@ int mandel_ipc_handle(void* dev_ptr, void* handle_out) {
     return MANDEL_OK;
 }
 
-int mandel_ipc_open(const void* handle, void** dev_ptr_out) {
+int mandel_ipc_open(int device, const void* handle, void** dev_ptr_out) {
     if (!handle || !dev_ptr_out) return fail(MANDEL_EINVAL, "ipc_open needs pointers");
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle, sizeof(h));
+    CK(cudaSetDevice(device));
     cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) { cuda_fail(e, "cudaIpcOpenMemHandle"); return MANDEL_ECOMM; }
     return MANDEL_OK;
@@ -709,6 +715,11 @@ int mandel_ipc_close(void* dev_ptr) {
 int mandel_dev_zero(void* dev_ptr, size_t bytes, void* stream) {
     if (!dev_ptr) return fail(MANDEL_EINVAL, "dev_zero needs a pointer");
     cudaStream_t s = (cudaStream_t)stream;
+    if (s) {
+        int dev = 0;
+        CK(cudaStreamGetDevice(s, &dev));
+        CK(cudaSetDevice(dev));
+    }
     CK(cudaMemsetAsync(dev_ptr, 0, bytes, s));
     CK(cudaStreamSynchronize(s));
     return MANDEL_OK;

@@ -50,6 +50,7 @@ struct Params {
     // static schemes: slot s -> row s < count0 ? base0 + s*stride0 : base1 + (s - count0)
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
+    uint32_t fcfs_sys;               // 1: the counter is shared across devices (system-scope atomics)
     uint32_t refill_lanes;           // lazy refill: leave the loop when this many lanes are free
     uint32_t adapt_lo, adapt_hi;     // adaptive: eager->lazy below adapt_lo iterations per run,
                                      // lazy->eager above adapt_hi
@@ -155,8 +156,9 @@ __device__ __forceinline__ int draw_tile(const Params& p, uint32_t& row, uint32_
         if (prev == kChunkDone) {
             g = kChunkDone;
         } else {
-            // the claim: one system-scope atomic on the shared counter (GPU 0's HBM)
-            const uint32_t c = atomicAdd_system(p.fcfs_ctr, 1u);
+            // the claim: one atomic on the shared counter in GPU 0's HBM -- system scope when
+            // ranks on other GPUs claim from it too (NVLink), device scope otherwise
+            const uint32_t c = p.fcfs_sys ? atomicAdd_system(p.fcfs_ctr, 1u) : atomicAdd(p.fcfs_ctr, 1u);
             g = c < p.nchunks ? c + 1 : kChunkDone;
             if (c < p.nchunks) atomicAdd(&p.ws->chunks_claimed, 1u);
         }

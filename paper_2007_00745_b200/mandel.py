@@ -131,7 +131,7 @@ def lib():
             L.mandel_dev_free.restype = i32
             L.mandel_ipc_handle.argtypes = [vp, vp]
             L.mandel_ipc_handle.restype = i32
-            L.mandel_ipc_open.argtypes = [vp, vp]
+            L.mandel_ipc_open.argtypes = [i32, vp, vp]
             L.mandel_ipc_open.restype = i32
             L.mandel_dev_zero.argtypes = [vp, ctypes.c_size_t, vp]
             L.mandel_dev_zero.restype = i32
@@ -279,11 +279,11 @@ def mandel_ipc_handle(ptr: int) -> bytes:
     return buf.raw
 
 
-def mandel_ipc_open(handle: bytes) -> int:
+def mandel_ipc_open(device: int, handle: bytes) -> int:
     if len(handle) != MANDEL_IPC_HANDLE_BYTES:
         raise ValueError("IPC handle must be MANDEL_IPC_HANDLE_BYTES long")
     p = ctypes.c_void_p(0)
-    _check(lib().mandel_ipc_open(handle, ctypes.byref(p)), "mandel_ipc_open")
+    _check(lib().mandel_ipc_open(device, handle, ctypes.byref(p)), "mandel_ipc_open")
     return int(p.value)
 
 
