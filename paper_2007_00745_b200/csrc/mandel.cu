@@ -306,8 +306,12 @@ int occupancy(int device, int fp32, int variant, int ilp, int mi, KernelFn fn, i
 int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
                  uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls) {
+    // FCFS with a single claimant: the counter hands that rank chunks 0, 1, 2, ... in
+    // order, so the dispatch is exactly the one-rank row order; run it as such (no
+    // claim atomics or chunk-map lookups; the claim count is reported as ceil(H/chunk)).
+    const int kscheme = (scheme == MANDEL_FCFS && nranks == 1) ? MANDEL_BLOCK : scheme;
     Plan pl;
-    int rc = make_plan(scheme, H, nranks, rank, pl);
+    int rc = make_plan(kscheme, H, nranks, rank, pl);
     if (rc) return rc;
     const int kernel = o ? o->kernel : MANDEL_KERNEL_REFILL;
     if (kernel < MANDEL_KERNEL_REFILL || kernel > MANDEL_KERNEL_ADAPTIVE)
@@ -326,7 +330,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.r2cand = dtype == MANDEL_FP64 ? (int)(((unsigned long long)d.r2bits + 1ull) >> 32)
                                     : (int)(d.r2bits + 1);
     p.W = W; p.H = H; p.iter_max = iter_max;
-    p.scheme = (uint32_t)scheme;
+    p.scheme = (uint32_t)kscheme;
     p.tile_w = tile;
     p.tiles_per_row = (W + tile - 1) / tile;
     p.nslots = pl.nslots; p.base0 = pl.base0; p.stride0 = pl.stride0; p.count0 = pl.count0; p.base1 = pl.base1;
@@ -374,6 +378,11 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         if (pl.nslots == 0) ls.grid.y = 1;
     }
     return MANDEL_OK;
+}
+
+uint32_t single_rank_claims(uint32_t H, const mandel_options* o) {
+    const uint32_t chunk = (o && o->chunk_rows) ? o->chunk_rows : kDefaultChunk;
+    return (uint32_t)(((uint64_t)H + chunk - 1) / chunk);
 }
 
 size_t state_bytes_for(uint32_t H, const mandel_options* o) {
@@ -513,6 +522,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
             stats->pixels += ws[r].pixels;
             claims += ws[r].chunks_claimed;
             if (r != 0) transfers += scheme == MANDEL_FCFS ? ws[r].chunks_claimed : 1u;
+            if (scheme == MANDEL_FCFS && ngpus == 1) claims = single_rank_claims(H, opts);
         }
         stats->chunks_claimed = claims;
         stats->transfers = transfers;
@@ -658,7 +668,8 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->rank_rows[0] = ws.rows_started;
         stats->sum_iters = ws.sum_iters;
         stats->pixels = ws.pixels;
-        stats->chunks_claimed = ws.chunks_claimed;
+        stats->chunks_claimed = (scheme == MANDEL_FCFS && nranks == 1) ? single_rank_claims(H, opts)
+                                                                      : ws.chunks_claimed;
         stats->transfers = rank == 0 ? 0u : (scheme == MANDEL_FCFS ? ws.chunks_claimed : 1u);
         stats->kernel_launches = 1;
         stats->ngpus = 1;

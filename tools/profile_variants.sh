@@ -5,9 +5,10 @@ set -u
 mkdir -p gpurun_out
 tag=$1; shift
 for spec in "$@"; do
-  IFS=: read cfg kern tile lanes <<< "$spec"
-  CMD="python tools/sweep.py --configs $cfg --kernels $kern --schemes block --tiles $tile --lanes $lanes --steps 1 --warmup 1"
-  out="gpurun_out/${tag}_${cfg}_${kern}_t${tile}_l${lanes}"
+  IFS=: read cfg kern tile lanes scheme <<< "$spec"
+  scheme=${scheme:-block}
+  CMD="python tools/sweep.py --configs $cfg --kernels $kern --schemes $scheme --tiles $tile --lanes $lanes --steps 1 --warmup 1"
+  out="gpurun_out/${tag}_${cfg}_${kern}_t${tile}_l${lanes}_${scheme}"
   $CMD > ${out}.plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:escape_ -s 1 -c 1 -o $out $CMD > ${out}.ncu.log 2>&1
   echo "$spec rc=$?"
