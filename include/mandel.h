@@ -32,6 +32,8 @@
  *   MANDEL_FCFS    "First Come First Served": GPUs claim
  *                  chunk_rows-row chunks from one atomic counter in GPU 0's
  *                  memory (system-scope atomics over NVLink); no master GPU.
+ *   MANDEL_FCFS_MASTER the paper's own FCFS: rank 0 computes nothing, the others
+ *                  claim single rows (Eq. 19: T_m = 2 iYmax messages) -- needs N >= 2.
  * Each GPU's kernel stores its counts directly into GPU 0's image (peer
  * stores over NVLink): the paper's "send to master" without a
  * separate gather or the alternating scheme's reconstruction pass.
@@ -59,7 +61,10 @@ enum mandel_dtype { MANDEL_FP64 = 0, MANDEL_FP32 = 1 };
 enum mandel_scheme {
     MANDEL_BLOCK = 0,   /* paper "Naive" row segmentation, Eq. 14-17     */
     MANDEL_CYCLIC = 1,  /* paper "Alternating" row segmentation          */
-    MANDEL_FCFS = 2     /* paper "First Come First Served" (chunked)     */
+    MANDEL_FCFS = 2,    /* paper "First Come First Served" (chunked)     */
+    MANDEL_FCFS_MASTER = 3  /* paper-faithful FCFS: rank 0 only
+                               dispatches and computes no rows; ranks 1..N-1 claim
+                               chunk_rows rows at a time (default 1 row); N >= 2 */
 };
 
 enum mandel_status {
@@ -95,8 +100,9 @@ typedef struct mandel_stats {
     uint64_t rank_pixels[MANDEL_MAX_GPUS]; /* per-rank pixels                                      */
     uint32_t rank_rows[MANDEL_MAX_GPUS];   /* per-rank rows started (FCFS: claimed chunk rows)     */
     uint32_t chunks_claimed;       /* FCFS successful global claims (= ceil(H/chunk_rows)); Eq. 19  */
-    uint32_t transfers;            /* rank->rank-0 result streams: N-1 (Eq. 18/20), FCFS: claims by
-                                      ranks != 0                                                     */
+    uint32_t transfers;            /* results sent to rank 0: static schemes one band per rank != 0
+                                      (N-1, Eq. 18/20); FCFS schemes the rows computed by ranks != 0
+                                      (FCFS_MASTER: every row; Eq. 19 counts claim + reply = 2 H)   */
     uint32_t kernel_launches;      /* kernels this call launched                                    */
     uint32_t ngpus;                /* ranks used                                                    */
     uint32_t ndevices;             /* distinct physical devices used                                */
@@ -132,7 +138,7 @@ typedef struct mandel_options {
  * EINVAL: W or H == 0; W*H*4 overflows size_t; iterMax == 0; R <= 0 or non-finite or
  *   R*R non-finite (in dtype); any bound non-finite (in dtype); xmin >= xmax or
  *   ymin >= ymax (after rounding, for fp32); dx or dy == 0 in dtype; dtype/scheme out of
- *   range; out_u32 == NULL; BLOCK/CYCLIC with H < ngpus.
+ *   range; out_u32 == NULL; BLOCK/CYCLIC with H < ngpus; FCFS_MASTER with ngpus < 2.
  * ENODEV: ngpus < 1, ngpus > devices, no CUDA device, or peer access unavailable.
  */
 int mandel_render(double xmin, double xmax, double ymin, double ymax,

@@ -108,6 +108,8 @@ struct Plan {
     uint32_t nslots, base0, stride0, count0, base1;
 };
 
+bool is_dynamic(int scheme) { return scheme == MANDEL_FCFS || scheme == MANDEL_FCFS_MASTER; }
+
 int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
     if (n < 1) return fail(MANDEL_EINVAL, "ngpus must be >= 1");
     if (r < 0 || r >= n) return fail(MANDEL_EINVAL, "rank out of range");
@@ -127,6 +129,11 @@ int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
         return MANDEL_OK;
     }
     if (scheme == MANDEL_FCFS) {
+        pl = Plan{0, 0, 0, 0, 0};
+        return MANDEL_OK;
+    }
+    if (scheme == MANDEL_FCFS_MASTER) {
+        if (N < 2) return fail(MANDEL_EINVAL, "FCFS_MASTER needs a master and at least one worker");
         pl = Plan{0, 0, 0, 0, 0};
         return MANDEL_OK;
     }
@@ -303,22 +310,39 @@ int occupancy(int device, int fp32, int variant, int ilp, int mi, KernelFn fn, i
     return MANDEL_OK;
 }
 
+// FCFS rows per claim: options.chunk_rows, else 16 (BASELINE.json C5) or, for the
+// paper's master/worker protocol, one row.  Sizes the chunk map too.
+uint32_t effective_chunk(int scheme, const mandel_options* o) {
+    if (o && o->chunk_rows) return o->chunk_rows;
+    return scheme == MANDEL_FCFS_MASTER ? 1u : kDefaultChunk;
+}
+
 int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
-                 uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls) {
+                 size_t state_cap, uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls) {
     // FCFS with a single claimant: the counter hands that rank chunks 0, 1, 2, ... in
     // order, so the dispatch is exactly the one-rank row order; run it as such (no
     // claim atomics or chunk-map lookups; the claim count is reported as ceil(H/chunk)).
-    const int kscheme = (scheme == MANDEL_FCFS && nranks == 1) ? MANDEL_BLOCK : scheme;
+    // FCFS_MASTER: rank 0 computes nothing (an empty plan, its kernel exits at once);
+    // the workers run the FCFS claim path with single-row chunks by default.
+    int kscheme = (scheme == MANDEL_FCFS && nranks == 1) ? MANDEL_BLOCK : scheme;
     Plan pl;
     int rc = make_plan(kscheme, H, nranks, rank, pl);
     if (rc) return rc;
+    if (kscheme == MANDEL_FCFS_MASTER) {
+        if (rank == 0) {
+            kscheme = MANDEL_BLOCK;
+            pl = Plan{0, 0, 1, 0, 0};
+        } else {
+            kscheme = MANDEL_FCFS;
+        }
+    }
     const int kernel = o ? o->kernel : MANDEL_KERNEL_REFILL;
     if (kernel < MANDEL_KERNEL_REFILL || kernel > MANDEL_KERNEL_ADAPTIVE)
         return fail(MANDEL_EINVAL, "options.kernel out of range");
-    if (kernel == MANDEL_KERNEL_STATIC && scheme == MANDEL_FCFS)
+    if (kernel == MANDEL_KERNEL_STATIC && is_dynamic(scheme))
         return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
-    const uint32_t chunk = (o && o->chunk_rows) ? o->chunk_rows : kDefaultChunk;
+    const uint32_t chunk = effective_chunk(scheme, o);
     uint32_t tile = (o && o->tile_px) ? o->tile_px : kDefaultTile;
     if (tile > W) tile = W;
     mandel::Params& p = ls.p;
@@ -336,13 +360,15 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.nslots = pl.nslots; p.base0 = pl.base0; p.stride0 = pl.stride0; p.count0 = pl.count0; p.base1 = pl.base1;
     p.chunk_rows = chunk;
     p.nchunks = (uint32_t)(((uint64_t)H + chunk - 1) / chunk);
-    if (scheme == MANDEL_FCFS) {
+    if (kscheme == MANDEL_FCFS) {
         uint64_t tiles = (uint64_t)(p.nchunks + 1) * chunk * p.tiles_per_row;
         if (tiles >= 0xF0000000ull) return fail(MANDEL_EINVAL, "FCFS tile space exceeds 32 bits; raise tile_px");
     } else if ((uint64_t)p.nslots * p.tiles_per_row >= 0xF0000000ull) {
         return fail(MANDEL_EINVAL, "tile space exceeds 32 bits; raise tile_px");
     }
     p.out = out;
+    if (sizeof(mandel::WorkState) + ((size_t)p.nchunks + 2) * sizeof(uint32_t) > state_cap)
+        return fail(MANDEL_ECUDA, "internal: chunk map larger than the rank state buffer");
     p.ws = reinterpret_cast<mandel::WorkState*>(state);
     p.chunk_map = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(state) + sizeof(mandel::WorkState));
     p.fcfs_ctr = fcfs_ctr;
@@ -381,12 +407,12 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
 }
 
 uint32_t single_rank_claims(uint32_t H, const mandel_options* o) {
-    const uint32_t chunk = (o && o->chunk_rows) ? o->chunk_rows : kDefaultChunk;
+    const uint32_t chunk = effective_chunk(MANDEL_FCFS, o);
     return (uint32_t)(((uint64_t)H + chunk - 1) / chunk);
 }
 
-size_t state_bytes_for(uint32_t H, const mandel_options* o) {
-    const uint32_t chunk = (o && o->chunk_rows) ? o->chunk_rows : kDefaultChunk;
+size_t state_bytes_for(int scheme, uint32_t H, const mandel_options* o) {
+    const uint32_t chunk = effective_chunk(scheme, o);
     const uint64_t nchunks = ((uint64_t)H + chunk - 1) / chunk;
     return sizeof(mandel::WorkState) + (nchunks + 2) * sizeof(uint32_t);
 }
@@ -410,11 +436,12 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     Derived d;
     int rc = derive(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, d);
     if (rc) return rc;
-    if (scheme < MANDEL_BLOCK || scheme > MANDEL_FCFS) return fail(MANDEL_EINVAL, "scheme out of range");
+    if (scheme < MANDEL_BLOCK || scheme > MANDEL_FCFS_MASTER) return fail(MANDEL_EINVAL, "scheme out of range");
     if (!out_host && !out_dev0) return fail(MANDEL_EINVAL, "need out_host or out_dev0");
+    if (scheme == MANDEL_FCFS_MASTER && ngpus < 2) return fail(MANDEL_EINVAL, "FCFS_MASTER needs ngpus >= 2");
     if (ngpus < 1 || ngpus > MANDEL_MAX_GPUS) return fail(MANDEL_ENODEV, "ngpus out of range");
-    if (scheme != MANDEL_FCFS && H < (uint32_t)ngpus) return fail(MANDEL_EINVAL, "static schemes need H >= ngpus");
-    if (opts && opts->kernel == MANDEL_KERNEL_STATIC && scheme == MANDEL_FCFS)
+    if (!is_dynamic(scheme) && H < (uint32_t)ngpus) return fail(MANDEL_EINVAL, "static schemes need H >= ngpus");
+    if (opts && opts->kernel == MANDEL_KERNEL_STATIC && is_dynamic(scheme))
         return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
     int ndev = 0;
     rc = device_count(ndev);
@@ -447,14 +474,14 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         }
         image = g_root.image;
     }
-    const size_t sbytes = state_bytes_for(H, opts);
+    const size_t sbytes = state_bytes_for(scheme, H, opts);
     std::vector<LaunchSpec> specs(ngpus);
     for (int r = 0; r < ngpus; ++r) {
         const int dev = r % ndev;
         rc = ensure_rank(r, dev, sbytes, nullptr);
         if (rc) return rc;
         rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, g_rank[r].state,
-                          g_root.fcfs_ctr, nphys > 1, dev, specs[r]);
+                          g_rank[r].state_bytes, g_root.fcfs_ctr, nphys > 1, dev, specs[r]);
         if (rc) return rc;
     }
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
@@ -521,7 +548,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
             stats->sum_iters += ws[r].sum_iters;
             stats->pixels += ws[r].pixels;
             claims += ws[r].chunks_claimed;
-            if (r != 0) transfers += scheme == MANDEL_FCFS ? ws[r].chunks_claimed : 1u;
+            if (r != 0) transfers += is_dynamic(scheme) ? ws[r].rows_started : 1u;
             if (scheme == MANDEL_FCFS && ngpus == 1) claims = single_rank_claims(H, opts);
         }
         stats->chunks_claimed = claims;
@@ -569,7 +596,7 @@ int mandel_device_count(void) {
 
 int mandel_plan_rows(int scheme, uint32_t H, int ngpus, int rank, uint32_t* rows_out, uint32_t* count) {
     if (!count) return fail(MANDEL_EINVAL, "count must not be NULL");
-    if (scheme == MANDEL_FCFS) return fail(MANDEL_EINVAL, "FCFS is dynamic: no static plan");
+    if (is_dynamic(scheme)) return fail(MANDEL_EINVAL, "FCFS is dynamic: no static plan");
     if (scheme != MANDEL_BLOCK && scheme != MANDEL_CYCLIC) return fail(MANDEL_EINVAL, "scheme out of range");
     Plan pl;
     int rc = make_plan(scheme, H, ngpus, rank, pl);
@@ -620,12 +647,13 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     Derived d;
     int rc = derive(xmin, xmax, ymin, ymax, W, H, iterMax, R, dtype, d);
     if (rc) return rc;
-    if (scheme < MANDEL_BLOCK || scheme > MANDEL_FCFS) return fail(MANDEL_EINVAL, "scheme out of range");
+    if (scheme < MANDEL_BLOCK || scheme > MANDEL_FCFS_MASTER) return fail(MANDEL_EINVAL, "scheme out of range");
+    if (scheme == MANDEL_FCFS_MASTER && nranks < 2) return fail(MANDEL_EINVAL, "FCFS_MASTER needs nranks >= 2");
     if (nranks < 1 || nranks > MANDEL_MAX_GPUS || rank < 0 || rank >= nranks)
         return fail(MANDEL_EINVAL, "rank/nranks out of range");
     if (!out_root) return fail(MANDEL_EINVAL, "out_root must not be NULL");
-    if (scheme == MANDEL_FCFS && !fcfs_counter) return fail(MANDEL_EINVAL, "FCFS needs fcfs_counter");
-    if (scheme != MANDEL_FCFS && H < (uint32_t)nranks) return fail(MANDEL_EINVAL, "static schemes need H >= nranks");
+    if (is_dynamic(scheme) && !fcfs_counter) return fail(MANDEL_EINVAL, "FCFS needs fcfs_counter");
+    if (!is_dynamic(scheme) && H < (uint32_t)nranks) return fail(MANDEL_EINVAL, "static schemes need H >= nranks");
     int ndev = 0;
     rc = device_count(ndev);
     if (rc) return rc;
@@ -636,7 +664,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     if (dev < 0 || dev >= ndev) return fail(MANDEL_ENODEV, "stream device out of range");
     rc = ensure_device(dev);
     if (rc) return rc;
-    const size_t sbytes = state_bytes_for(H, opts);
+    const size_t sbytes = state_bytes_for(scheme, H, opts);
     // slot 0 of the rank table holds this process's single rank
     rc = ensure_rank(0, dev, sbytes, nullptr);
     if (rc) return rc;
@@ -644,7 +672,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     LaunchSpec ls;
     // across processes the counter is (in general) on another GPU: system scope
     rc = build_params(d, W, H, iterMax, dtype, scheme, nranks, rank, opts, out_root, rk.state,
-                      fcfs_counter, nranks > 1, dev, ls);
+                      rk.state_bytes, fcfs_counter, nranks > 1, dev, ls);
     if (rc) return rc;
     cudaStream_t s = streamv ? (cudaStream_t)streamv : rk.stream;
     const double t0 = now_ms();
@@ -670,7 +698,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->pixels = ws.pixels;
         stats->chunks_claimed = (scheme == MANDEL_FCFS && nranks == 1) ? single_rank_claims(H, opts)
                                                                       : ws.chunks_claimed;
-        stats->transfers = rank == 0 ? 0u : (scheme == MANDEL_FCFS ? ws.chunks_claimed : 1u);
+        stats->transfers = rank == 0 ? 0u : (is_dynamic(scheme) ? ws.rows_started : 1u);
         stats->kernel_launches = 1;
         stats->ngpus = 1;
         stats->ndevices = 1;

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libmandel.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "mandel.h")
 
 MANDEL_FP64, MANDEL_FP32 = 0, 1
-MANDEL_BLOCK, MANDEL_CYCLIC, MANDEL_FCFS = 0, 1, 2
+MANDEL_BLOCK, MANDEL_CYCLIC, MANDEL_FCFS, MANDEL_FCFS_MASTER = 0, 1, 2, 3
 MANDEL_OK, MANDEL_EINVAL, MANDEL_ENODEV, MANDEL_ENOMEM = 0, -1, -2, -3
 MANDEL_ECUDA, MANDEL_ECOMM, MANDEL_EBUSY = -4, -5, -6
 MANDEL_KERNEL_REFILL, MANDEL_KERNEL_STATIC, MANDEL_KERNEL_EAGER, MANDEL_KERNEL_LAZY = 0, 1, 2, 3
@@ -34,7 +34,7 @@ MANDEL_IPC_HANDLE_BYTES = 64
 
 DTYPES = {"fp64": MANDEL_FP64, "fp32": MANDEL_FP32}
 SCHEMES = {"block": MANDEL_BLOCK, "naive": MANDEL_BLOCK, "cyclic": MANDEL_CYCLIC,
-           "alternating": MANDEL_CYCLIC, "fcfs": MANDEL_FCFS}
+           "alternating": MANDEL_CYCLIC, "fcfs": MANDEL_FCFS, "fcfs_master": MANDEL_FCFS_MASTER}
 
 
 class MandelError(RuntimeError):

@@ -62,7 +62,7 @@ class RankRenderer:
 
     def step(self, scheme: str, **kw) -> dict:
         """One render: reset the shared counter (FCFS), line up, render, line up."""
-        if M.SCHEMES[scheme] == M.MANDEL_FCFS and self.rank == 0:
+        if M.SCHEMES[scheme] in (M.MANDEL_FCFS, M.MANDEL_FCFS_MASTER) and self.rank == 0:
             M.mandel_dev_zero(self.ctr, self.CTR_BYTES, self.stream)
         self.dist.barrier()
         st = M.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world, self.img,

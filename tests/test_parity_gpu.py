@@ -127,6 +127,21 @@ def test_edge_cases(mandel, oracle, cfg, scheme, kernel):
         assert st["pixels"] == cfg.pixels
 
 
+@pytest.mark.parametrize("ngpus", [2, 3, 5, 8])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_fcfs_master_worker(mandel, oracle, ngpus, dtype):
+    # the paper's FCFS: the master computes no rows, workers claim rows
+    cfg = wl.C1.with_(dtype=dtype, W=517, H=301)
+    out, st = _render_dev(mandel, cfg, "fcfs_master", ngpus)
+    _assert_same(_host(out), oracle.render(cfg), f"fcfs_master/N={ngpus}")
+    assert st["rank_rows"][0] == 0 and st["rank_pixels"][0] == 0
+    assert sum(st["rank_rows"]) == cfg.H
+    assert st["chunks_claimed"] == cfg.H          # one claim per row
+    assert st["transfers"] == cfg.H               # every row is sent to the master (Eq. 19: 2 H)
+    if ngpus == 2:
+        assert st["rank_rows"][1] == cfg.H        # one worker does everything
+
+
 def test_fcfs_more_ranks_than_rows(mandel, oracle):
     cfg = wl.Config("fewrows", -2.5, 1.5, -2.0, 2.0, 300, 3, 200, 2.0, "fp64")
     out, st = _render_dev(mandel, cfg, "fcfs", 8, chunk_rows=1)

@@ -92,3 +92,5 @@ def test_library_plan_errors(mandel):
         mandel.mandel_plan_rows(mandel.MANDEL_FCFS, 100, 2, 0)  # dynamic: no static plan
     with pytest.raises(mandel.MandelError):
         mandel.mandel_plan_rows(mandel.MANDEL_CYCLIC, 100, 2, 2)
+    with pytest.raises(mandel.MandelError):
+        mandel.mandel_plan_rows(mandel.MANDEL_FCFS_MASTER, 100, 4, 1)
