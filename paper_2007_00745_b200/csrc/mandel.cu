@@ -158,11 +158,18 @@ struct RankCtx {
     size_t state_bytes = 0;
 };
 
+constexpr int kMaxBands = 32;
+
 struct Root {
     uint32_t* image = nullptr;  // library-owned map on device 0
     size_t image_bytes = 0;
     uint32_t* fcfs_ctr = nullptr;
     cudaEvent_t start = nullptr, done = nullptr, d2h = nullptr;
+    // pipelined one-GPU hand-off: band states, a second compute stream, a copy stream
+    void* band_state = nullptr;
+    size_t band_state_bytes = 0;
+    cudaStream_t band_stream = nullptr, copy_stream = nullptr;
+    cudaEvent_t band_k0[kMaxBands] = {}, band_k1[kMaxBands] = {}, band_cp[kMaxBands] = {};
 };
 
 std::mutex g_mu;
@@ -223,6 +230,7 @@ constexpr KernelChoice kDefaultChoice[2] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp
                                             {MANDEL_KERNEL_EAGER, 4, 1}};  // fp32: C3 53.8% (issue-bound)
 constexpr uint32_t kDefaultRefillLanes = 8;
 constexpr uint32_t kDefaultAdaptLo = 16, kDefaultAdaptHi = 64;
+constexpr int kDefaultBands = 8;  // C2: 4 -> 8.50 ms, 8 -> 8.29 ms, 16 -> 8.86 ms per render (e2e_probe)  // pipelined device->host hand-off (one GPU, host output)
 
 int device_count(int& n) {
     n = 0;
@@ -319,7 +327,8 @@ uint32_t effective_chunk(int scheme, const mandel_options* o) {
 
 int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
-                 size_t state_cap, uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls) {
+                 size_t state_cap, uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls,
+                 const Plan* band = nullptr) {
     // FCFS with a single claimant: the counter hands that rank chunks 0, 1, 2, ... in
     // order, so the dispatch is exactly the one-rank row order; run it as such (no
     // claim atomics or chunk-map lookups; the claim count is reported as ceil(H/chunk)).
@@ -329,6 +338,10 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     Plan pl;
     int rc = make_plan(kscheme, H, nranks, rank, pl);
     if (rc) return rc;
+    if (band) {  // a row band of a one-GPU render (pipelined hand-off): rows in order
+        kscheme = MANDEL_BLOCK;
+        pl = *band;
+    }
     if (kscheme == MANDEL_FCFS_MASTER) {
         if (rank == 0) {
             kscheme = MANDEL_BLOCK;
@@ -428,6 +441,101 @@ double now_ms() {
     return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
+// One GPU with a host destination: split the rows into `bands` bands, launch them
+// alternately on two streams (a band's kernel fills the previous band's tail), and
+// copy each finished band to the host on a copy stream while later bands compute --
+// the paper's master file write overlapped with generation.
+int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
+                  const mandel_options* opts, uint32_t* image, uint32_t* out_host, void* stream0v,
+                  mandel_stats* stats, int bands, size_t sbytes, double t_call) {
+    int rc = ensure_rank(0, 0, sbytes, nullptr);
+    if (rc) return rc;
+    CK(cudaSetDevice(0));
+    const size_t need = sbytes * (size_t)bands;
+    if (g_root.band_state_bytes < need) {
+        if (g_root.band_state) CK(cudaFree(g_root.band_state));
+        g_root.band_state = nullptr;
+        g_root.band_state_bytes = 0;
+        CK(cudaMalloc(&g_root.band_state, need));
+        g_root.band_state_bytes = need;
+    }
+    if (!g_root.band_stream) CK(cudaStreamCreateWithFlags(&g_root.band_stream, cudaStreamDefault));
+    if (!g_root.copy_stream) CK(cudaStreamCreateWithFlags(&g_root.copy_stream, cudaStreamDefault));
+    for (int b = 0; b < bands; ++b) {
+        if (!g_root.band_k0[b]) CK(cudaEventCreate(&g_root.band_k0[b]));
+        if (!g_root.band_k1[b]) CK(cudaEventCreate(&g_root.band_k1[b]));
+        if (!g_root.band_cp[b]) CK(cudaEventCreate(&g_root.band_cp[b]));
+    }
+    std::vector<LaunchSpec> specs(bands);
+    std::vector<uint32_t> r0(bands), nr(bands);
+    for (int b = 0; b < bands; ++b) {
+        r0[b] = (uint32_t)((uint64_t)H * b / bands);
+        nr[b] = (uint32_t)((uint64_t)H * (b + 1) / bands) - r0[b];
+        Plan pl{nr[b], r0[b], 1, nr[b], 0};
+        char* st = reinterpret_cast<char*>(g_root.band_state) + sbytes * b;
+        rc = build_params(d, W, H, iter_max, dtype, scheme, 1, 0, opts, image, st, sbytes,
+                          g_root.fcfs_ctr, false, 0, specs[b], &pl);
+        if (rc) return rc;
+    }
+    cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
+    cudaStream_t cs[2] = {s0, g_root.band_stream};
+    cudaStream_t cp = g_root.copy_stream;
+    CK(cudaMemsetAsync(g_root.band_state, 0, need, s0));
+    CK(cudaEventRecord(g_root.start, s0));
+    CK(cudaStreamWaitEvent(cs[1], g_root.start, 0));
+    CK(cudaStreamWaitEvent(cp, g_root.start, 0));
+    // outside-in band order (0, B-1, 1, B-2, ...): the edges of a view are usually the
+    // cheap rows, so their copies drain while the costly middle bands still compute
+    for (int i = 0; i < bands; ++i) {
+        const int b = (i & 1) ? bands - 1 - i / 2 : i / 2;
+        cudaStream_t s = cs[i & 1];
+        CK(cudaEventRecord(g_root.band_k0[b], s));
+        rc = launch(specs[b], s);
+        if (rc) return rc;
+        CK(cudaEventRecord(g_root.band_k1[b], s));
+        CK(cudaStreamWaitEvent(cp, g_root.band_k1[b], 0));
+        const size_t off = (size_t)r0[b] * W;
+        CK(cudaMemcpyAsync(out_host + off, image + off, (size_t)nr[b] * W * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, cp));
+        CK(cudaEventRecord(g_root.band_cp[b], cp));
+    }
+    // s0 (the caller's stream) is done when every band kernel and every copy is
+    for (int b = 0; b < bands; ++b) CK(cudaStreamWaitEvent(s0, g_root.band_k1[b], 0));
+    const int last = (bands & 1) ? (bands - 1) / 2 : bands / 2;  // last band issued
+    CK(cudaStreamWaitEvent(s0, g_root.band_cp[last], 0));
+    CK(cudaEventRecord(g_root.d2h, s0));
+    std::vector<mandel::WorkState> ws(bands);
+    for (int b = 0; b < bands; ++b)
+        CK(cudaMemcpyAsync(&ws[b], reinterpret_cast<char*>(g_root.band_state) + sbytes * b,
+                           sizeof(mandel::WorkState), cudaMemcpyDeviceToHost, s0));
+    CK(cudaStreamSynchronize(s0));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        float ms = 0, kend = 0;
+        for (int b = 0; b < bands; ++b) {
+            CK(cudaEventElapsedTime(&ms, g_root.start, g_root.band_k1[b]));
+            if (ms > kend) kend = ms;
+            stats->sum_iters += ws[b].sum_iters;
+            stats->pixels += ws[b].pixels;
+            stats->rank_rows[0] += ws[b].rows_started;
+        }
+        stats->device_ms = kend;
+        stats->kernel_ms[0] = kend;
+        stats->kernel_ms_max = kend;
+        CK(cudaEventElapsedTime(&ms, g_root.start, g_root.d2h));
+        stats->d2h_ms = ms - kend;  // the part of the hand-off not hidden behind compute
+        stats->rank_iters[0] = stats->sum_iters;
+        stats->rank_pixels[0] = stats->pixels;
+        stats->chunks_claimed = is_dynamic(scheme) ? single_rank_claims(H, opts) : 0u;
+        stats->transfers = 0;
+        stats->kernel_launches = (uint32_t)bands;
+        stats->ngpus = 1;
+        stats->ndevices = 1;
+        stats->total_ms = now_ms() - t_call;
+    }
+    return MANDEL_OK;
+}
+
 int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
                 uint32_t iter_max, double R, int dtype, int scheme, int ngpus,
                 const mandel_options* opts, uint32_t* out_host, uint32_t* out_dev0,
@@ -475,6 +583,10 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         image = g_root.image;
     }
     const size_t sbytes = state_bytes_for(scheme, H, opts);
+    const int bands = opts && opts->bands ? opts->bands : kDefaultBands;
+    if (out_host && ngpus == 1 && bands > 1 && H >= 2 * (uint32_t)bands && scheme != MANDEL_FCFS_MASTER)
+        return render_banded(d, W, H, iter_max, dtype, scheme, opts, image, out_host, stream0v,
+                             stats, bands > kMaxBands ? kMaxBands : bands, sbytes, t_call);
     std::vector<LaunchSpec> specs(ngpus);
     for (int r = 0; r < ngpus; ++r) {
         const int dev = r % ndev;
@@ -783,6 +895,14 @@ void mandel_shutdown(void) {
         if (g_root.start) cudaEventDestroy(g_root.start);
         if (g_root.done) cudaEventDestroy(g_root.done);
         if (g_root.d2h) cudaEventDestroy(g_root.d2h);
+        if (g_root.band_state) cudaFree(g_root.band_state);
+        if (g_root.band_stream) cudaStreamDestroy(g_root.band_stream);
+        if (g_root.copy_stream) cudaStreamDestroy(g_root.copy_stream);
+        for (int b = 0; b < kMaxBands; ++b) {
+            if (g_root.band_k0[b]) cudaEventDestroy(g_root.band_k0[b]);
+            if (g_root.band_k1[b]) cudaEventDestroy(g_root.band_k1[b]);
+            if (g_root.band_cp[b]) cudaEventDestroy(g_root.band_cp[b]);
+        }
     }
     g_root = Root();
     for (auto& d : g_dev) d.init = false;

@@ -88,6 +88,7 @@ class mandel_options(ctypes.Structure):
         ("min_ctas", ctypes.c_int),
         ("adapt_lo", ctypes.c_int),
         ("adapt_hi", ctypes.c_int),
+        ("bands", ctypes.c_int),
     ]
 
 
@@ -177,7 +178,7 @@ def _ptr(a) -> int | None:
 
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
-          refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0):
+          refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -188,6 +189,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.min_ctas = min_ctas or 0
     o.adapt_lo = adapt_lo or 0
     o.adapt_hi = adapt_hi or 0
+    o.bands = bands or 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -217,13 +219,14 @@ def mandel_render(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, ngpu
 def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", scheme="block",
                      ngpus=1, *, out_host=None, out_dev0=None, stream0=None, chunk_rows=0,
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
-                     refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0) -> dict:
+                     refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
+                     bands=0) -> dict:
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict."""
     st = mandel_stats()
     o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
-              adapt_hi)
+              adapt_hi, bands)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st))

@@ -159,6 +159,18 @@ def test_host_output_entry_point(mandel, oracle):
     assert st["d2h_ms"] > 0
 
 
+@pytest.mark.parametrize("bands", [0, 1, 2, 3, 7, 32])
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_pipelined_host_output(mandel, oracle, bands, scheme):
+    # one GPU + host destination: row bands copied to the host while later bands compute
+    cfg = wl.C1.with_(W=333, H=251, iter_max=700)
+    want = oracle.render(cfg)
+    got, st = mandel.render(*cfg.args(), "fp64", scheme, 1, bands=bands)
+    _assert_same(got, want, f"bands={bands}/{scheme}")
+    assert st["sum_iters"] == int(want.sum(dtype=np.uint64)) and st["pixels"] == cfg.pixels
+    assert st["kernel_launches"] == (1 if bands == 1 else (bands or 8))
+
+
 def test_repeat_is_deterministic(mandel):
     cfg = wl.C1.with_(iter_max=1000)
     a, _ = _render_dev(mandel, cfg, "fcfs", 1)
