@@ -74,8 +74,11 @@ enum mandel_status {
     MANDEL_ENOMEM = -3,  /* device or pinned allocation failed                         */
     MANDEL_ECUDA = -4,   /* a CUDA runtime call failed (detail: mandel_last_error)      */
     MANDEL_ECOMM = -5,   /* inter-GPU / inter-process plumbing failed (IPC, peer map)   */
-    MANDEL_EBUSY = -6    /* another call is in progress                                */
+    MANDEL_EBUSY = -6,   /* another call is in progress                                */
+    MANDEL_EIO = -7      /* a file could not be written (mandel_write_ppm)             */
 };
+
+enum mandel_colour { MANDEL_COLOUR_GRAY = 0, MANDEL_COLOUR_CLASSIC = 1 };
 
 enum mandel_kernel {
     MANDEL_KERNEL_REFILL = 0,  /* default: the fastest measured configuration for the dtype      */
@@ -217,6 +220,24 @@ int mandel_dev_zero(void *dev_ptr, size_t bytes, void *stream);
  */
 int mandel_plan_rows(int scheme, uint32_t H, int ngpus, int rank,
                      uint32_t *rows_out, uint32_t *count);
+
+/*
+ * Output stage (after the hot path; "The iteration is then used to determine
+ * the pixel color", PAPER.md:179 the master writes the image file).  The paper names no
+ * palette: MANDEL_COLOUR_GRAY is SPEC.md:313-321's ramp (interior n == iterMax black,
+ * escaped v = round-half-up(255 (n-1)/(iterMax-1)) in all three channels);
+ * MANDEL_COLOUR_CLASSIC is (7n, 13n, 29n) mod 256 for escaped pixels, interior black.
+ * mandel_colorize: counts_dev (W*H uint32, device) -> rgb_dev (3*W*H bytes, device,
+ *   r, g, b per pixel, row-major), on `stream` (nullable: legacy default stream of the
+ *   pointer's device); returns when done.  EINVAL on NULL pointers, W or H == 0,
+ *   iterMax == 0 or an unknown mode.
+ * mandel_write_ppm: binary PPM (P6) "P6\n<W> <H>\n255\n" + rgb_host (3*W*H bytes, host)
+ *   to `path`; *bytes_written (nullable) = header + 3*W*H.  EINVAL / EIO.
+ */
+int mandel_colorize(const uint32_t *counts_dev, uint8_t *rgb_dev, uint32_t W, uint32_t H,
+                    uint32_t iterMax, int mode, void *stream);
+int mandel_write_ppm(const char *path, const uint8_t *rgb_host, uint32_t W, uint32_t H,
+                     uint64_t *bytes_written);
 
 /* Static description of a status code (never NULL). */
 const char *mandel_strerror(int code);

@@ -15,7 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmandel.so")
 SOURCES = [os.path.join(CSRC, "mandel.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "mandel_kernels.cuh"), os.path.join(ROOT, "include", "mandel.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "mandel_kernels.cuh"), os.path.join(CSRC, "mandel_image.cuh"),
+                  os.path.join(ROOT, "include", "mandel.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -17,6 +17,7 @@
 
 #include "mandel.h"
 #include "mandel_kernels.cuh"
+#include "mandel_image.cuh"
 
 namespace {
 
@@ -691,6 +692,7 @@ const char* mandel_strerror(int code) {
         case MANDEL_ECUDA: return "CUDA runtime error";
         case MANDEL_ECOMM: return "inter-GPU communication error";
         case MANDEL_EBUSY: return "library busy (concurrent call)";
+        case MANDEL_EIO: return "file write failed";
         default: return "unknown status";
     }
 }
@@ -860,6 +862,47 @@ int mandel_ipc_close(void* dev_ptr) {
     if (!dev_ptr) return fail(MANDEL_EINVAL, "ipc_close needs a pointer");
     cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
     if (e != cudaSuccess) { cuda_fail(e, "cudaIpcCloseMemHandle"); return MANDEL_ECOMM; }
+    return MANDEL_OK;
+}
+
+int mandel_colorize(const uint32_t* counts_dev, uint8_t* rgb_dev, uint32_t W, uint32_t H,
+                    uint32_t iterMax, int mode, void* stream) {
+    if (!counts_dev || !rgb_dev) return fail(MANDEL_EINVAL, "colorize needs device pointers");
+    if (W == 0 || H == 0 || iterMax == 0) return fail(MANDEL_EINVAL, "colorize needs W, H, iterMax >= 1");
+    if (mode != MANDEL_COLOUR_GRAY && mode != MANDEL_COLOUR_CLASSIC) return fail(MANDEL_EINVAL, "unknown colour mode");
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    if (s) CK(cudaStreamGetDevice(s, &dev));
+    else {
+        cudaPointerAttributes a;
+        CK(cudaPointerGetAttributes(&a, counts_dev));
+        dev = a.device;
+    }
+    CK(cudaSetDevice(dev));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t npix = (uint64_t)W * H;
+    const bool aligned = ((uintptr_t)counts_dev % 16 == 0) && ((uintptr_t)rgb_dev % 4 == 0);
+    const unsigned grid = (unsigned)(sms * 8);  // 8 x 256-thread CTAs per SM, grid-stride
+    if (aligned) mandel::colourize_kernel<<<grid, 256, 0, s>>>(counts_dev, rgb_dev, npix, iterMax, mode);
+    else mandel::colourize_scalar_kernel<<<grid, 256, 0, s>>>(counts_dev, rgb_dev, npix, iterMax, mode);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return MANDEL_OK;
+}
+
+int mandel_write_ppm(const char* path, const uint8_t* rgb_host, uint32_t W, uint32_t H,
+                     uint64_t* bytes_written) {
+    if (!path || !rgb_host || W == 0 || H == 0) return fail(MANDEL_EINVAL, "write_ppm needs a path, data and W, H >= 1");
+    char hdr[64];
+    const int hl = std::snprintf(hdr, sizeof(hdr), "P6\n%u %u\n255\n", W, H);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return fail(MANDEL_EIO, std::string("cannot open ") + path);
+    const size_t body = (size_t)W * H * 3;
+    bool ok = std::fwrite(hdr, 1, (size_t)hl, f) == (size_t)hl && std::fwrite(rgb_host, 1, body, f) == body;
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) return fail(MANDEL_EIO, std::string("write failed: ") + path);
+    if (bytes_written) *bytes_written = (uint64_t)hl + body;
     return MANDEL_OK;
 }
 

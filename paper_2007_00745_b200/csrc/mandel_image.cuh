@@ -1,0 +1,74 @@
+// mandel_image.cuh -- output stage after the hot path: iteration counts -> RGB bytes.
+//
+// "The iteration is then used to determine the pixel color in the image
+// I"; the paper names no palette, so the palettes follow SPEC.md:313-321 (grayscale,
+// invented) and an integer "classic" palette.  Integer arithmetic
+// only, so the bytes are exact and the oracle (oracle/colour.py) can match them.
+//   interior (n == iterMax)      -> (0, 0, 0)                         both modes
+//   grayscale, escaped           -> v = round_half_up(255 (n-1) / (iterMax-1)), (v,v,v)
+//   classic, escaped             -> (7n mod 256, 13n mod 256, 29n mod 256)
+// HBM-bound: 4 B read + 3 B written per pixel; 4 pixels per thread per step with a
+// 16-B load and three 4-B stores (12 B of RGB), grid-stride over the map.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mandel {
+
+enum : int { kColorGray = 0, kColorClassic = 1 };
+
+__device__ __forceinline__ uint32_t colour_rgb(uint32_t n, uint32_t iter_max, int mode) {
+    if (n >= iter_max) return 0u;
+    uint32_t r, g, b;
+    if (mode == kColorGray) {
+        // round(255 (n-1) / (M-1)) half up, in 64-bit integers (M >= 2 here)
+        const uint64_t den = 2ull * (iter_max - 1);
+        const uint32_t v = (uint32_t)((510ull * (n - 1) + (iter_max - 1)) / den);
+        r = g = b = v;
+    } else {
+        r = (7u * n) & 255u;
+        g = (13u * n) & 255u;
+        b = (29u * n) & 255u;
+    }
+    return r | (g << 8) | (b << 16);  // bytes r, g, b (little-endian)
+}
+
+__global__ void colourize_kernel(const uint32_t* __restrict__ counts, uint8_t* __restrict__ rgb,
+                                 uint64_t npix, uint32_t iter_max, int mode) {
+    const uint64_t ngroups = npix / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+        const uint4 c = reinterpret_cast<const uint4*>(counts)[g];
+        const uint32_t p0 = colour_rgb(c.x, iter_max, mode), p1 = colour_rgb(c.y, iter_max, mode);
+        const uint32_t p2 = colour_rgb(c.z, iter_max, mode), p3 = colour_rgb(c.w, iter_max, mode);
+        // 4 pixels x 3 bytes = 12 bytes = three little-endian words
+        uint32_t* o = reinterpret_cast<uint32_t*>(rgb + 12 * g);
+        o[0] = p0 | (p1 << 24);
+        o[1] = (p1 >> 8) | (p2 << 16);
+        o[2] = (p2 >> 16) | (p3 << 8);
+    }
+    // tail pixels (npix mod 4), one thread each
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t rem = npix - ngroups * 4;
+    if (t < rem) {
+        const uint64_t i = ngroups * 4 + t;
+        const uint32_t p = colour_rgb(counts[i], iter_max, mode);
+        rgb[3 * i] = (uint8_t)p;
+        rgb[3 * i + 1] = (uint8_t)(p >> 8);
+        rgb[3 * i + 2] = (uint8_t)(p >> 16);
+    }
+}
+
+// unaligned fallback: one pixel per thread per step
+__global__ void colourize_scalar_kernel(const uint32_t* __restrict__ counts, uint8_t* __restrict__ rgb,
+                                        uint64_t npix, uint32_t iter_max, int mode) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npix; i += stride) {
+        const uint32_t p = colour_rgb(counts[i], iter_max, mode);
+        rgb[3 * i] = (uint8_t)p;
+        rgb[3 * i + 1] = (uint8_t)(p >> 8);
+        rgb[3 * i + 2] = (uint8_t)(p >> 16);
+    }
+}
+
+}  // namespace mandel

@@ -21,7 +21,9 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "mandel.h")
 MANDEL_FP64, MANDEL_FP32 = 0, 1
 MANDEL_BLOCK, MANDEL_CYCLIC, MANDEL_FCFS, MANDEL_FCFS_MASTER = 0, 1, 2, 3
 MANDEL_OK, MANDEL_EINVAL, MANDEL_ENODEV, MANDEL_ENOMEM = 0, -1, -2, -3
-MANDEL_ECUDA, MANDEL_ECOMM, MANDEL_EBUSY = -4, -5, -6
+MANDEL_ECUDA, MANDEL_ECOMM, MANDEL_EBUSY, MANDEL_EIO = -4, -5, -6, -7
+MANDEL_COLOUR_GRAY, MANDEL_COLOUR_CLASSIC = 0, 1
+COLOURS = {"gray": MANDEL_COLOUR_GRAY, "grey": MANDEL_COLOUR_GRAY, "classic": MANDEL_COLOUR_CLASSIC}
 MANDEL_KERNEL_REFILL, MANDEL_KERNEL_STATIC, MANDEL_KERNEL_EAGER, MANDEL_KERNEL_LAZY = 0, 1, 2, 3
 MANDEL_KERNEL_ADAPTIVE = 4
 # name -> (mandel_kernel, ilp); ilp 0 = the library's default for that kernel
@@ -134,6 +136,10 @@ def lib():
             L.mandel_ipc_handle.restype = i32
             L.mandel_ipc_open.argtypes = [i32, vp, vp]
             L.mandel_ipc_open.restype = i32
+            L.mandel_colorize.argtypes = [vp, vp, u32, u32, u32, i32, vp]
+            L.mandel_colorize.restype = i32
+            L.mandel_write_ppm.argtypes = [ctypes.c_char_p, vp, u32, u32, vp]
+            L.mandel_write_ppm.restype = i32
             L.mandel_dev_zero.argtypes = [vp, ctypes.c_size_t, vp]
             L.mandel_dev_zero.restype = i32
             L.mandel_ipc_close.argtypes = [vp]
@@ -292,6 +298,20 @@ def mandel_ipc_open(device: int, handle: bytes) -> int:
 
 def mandel_ipc_close(ptr: int) -> None:
     _check(lib().mandel_ipc_close(ptr), "mandel_ipc_close")
+
+
+def mandel_colorize(counts_dev, rgb_dev, W, H, iter_max, mode="gray", stream=None) -> None:
+    """C: mandel_colorize (device counts -> device RGB bytes)."""
+    _check(lib().mandel_colorize(_ptr(counts_dev), _ptr(rgb_dev), W, H, iter_max,
+                                 _enum(mode, COLOURS), stream), "mandel_colorize")
+
+
+def mandel_write_ppm(path: str, rgb_host, W: int, H: int) -> int:
+    """C: mandel_write_ppm (binary P6); returns the bytes written."""
+    n = ctypes.c_uint64(0)
+    _check(lib().mandel_write_ppm(os.fsencode(path), _ptr(rgb_host), W, H, ctypes.byref(n)),
+           "mandel_write_ppm")
+    return int(n.value)
 
 
 def render(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", scheme="block", ngpus=1,
