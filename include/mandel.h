@@ -56,7 +56,13 @@ extern "C" {
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
-enum mandel_dtype { MANDEL_FP64 = 0, MANDEL_FP32 = 1 };
+enum mandel_dtype {
+    MANDEL_FP64 = 0,     /* the reference map: every operation a separate RN double op          */
+    MANDEL_FP32 = 1,     /* the same in float (bounds and R rounded to float first)             */
+    MANDEL_FP64_FMA = 2  /* double with fused multiply-adds in the iteration (R17):
+                            y' = fma(x+x, y, ci); x' = fma(x, x, -y^2) + cr; |z|^2 = fma(x', x', y'^2)
+                            -- 6 instead of 8 FP64 instructions; a different, equally exact map */
+};
 
 enum mandel_scheme {
     MANDEL_BLOCK = 0,   /* paper "Naive" row segmentation, Eq. 14-17     */

@@ -30,12 +30,13 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 FP64 = 0
 FP32 = 1
+FP64_FMA = 2
 
 _lib = None
 _lock = threading.Lock()
 
 BUILD_CMD = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math",
-             "-fPIC", "-shared", "-o", _LIB_PATH, _SRC]
+             "-fPIC", "-shared", "-o", _LIB_PATH, _SRC, "-lm"]
 
 
 def build(force: bool = False) -> str:
@@ -55,6 +56,8 @@ def lib():
             u32, f64, f32, i32 = ctypes.c_uint32, ctypes.c_double, ctypes.c_float, ctypes.c_int
             L.oracle_escape_f64.argtypes = [f64, f64, u32, f64]
             L.oracle_escape_f64.restype = u32
+            L.oracle_escape_f64fma.argtypes = [f64, f64, u32, f64]
+            L.oracle_escape_f64fma.restype = u32
             L.oracle_escape_f32.argtypes = [f32, f32, u32, f32]
             L.oracle_escape_f32.restype = u32
             L.oracle_derive_f64.argtypes = [f64, f64, f64, f64, u32, u32, f64, ctypes.c_void_p]
@@ -82,6 +85,8 @@ def _dt(dtype) -> int:
         return FP64
     if dtype in (FP32, "fp32", "f32", "float32"):
         return FP32
+    if dtype in (FP64_FMA, "fp64fma"):
+        return FP64_FMA
     raise ValueError(f"unknown dtype {dtype!r}")
 
 
@@ -90,6 +95,8 @@ def escape(cr: float, ci: float, iter_max: int, R: float, dtype="fp64") -> int:
     L = lib()
     if _dt(dtype) == FP64:
         return int(L.oracle_escape_f64(cr, ci, iter_max, R * R))
+    if _dt(dtype) == FP64_FMA:
+        return int(L.oracle_escape_f64fma(cr, ci, iter_max, R * R))
     rf = float(np.float32(R))
     r2 = float(np.float32(rf) * np.float32(rf))
     return int(L.oracle_escape_f32(float(np.float32(cr)), float(np.float32(ci)), iter_max, r2))
@@ -98,7 +105,7 @@ def escape(cr: float, ci: float, iter_max: int, R: float, dtype="fp64") -> int:
 def derive(xmin, xmax, ymin, ymax, W, H, R, dtype="fp64"):
     """Step a1: (dx, dy, R2) in fp64, or (xmin_f, ymax_f, dx, dy, R2) in fp32."""
     L = lib()
-    if _dt(dtype) == FP64:
+    if _dt(dtype) in (FP64, FP64_FMA):
         out = (ctypes.c_double * 3)()
         L.oracle_derive_f64(xmin, xmax, ymin, ymax, W, H, R, ctypes.addressof(out))
         return tuple(out)
@@ -110,7 +117,7 @@ def derive(xmin, xmax, ymin, ymax, W, H, R, dtype="fp64"):
 def axes(xmin, xmax, ymin, ymax, W, H, R, dtype="fp64"):
     """Step a3: the Cx and Cy arrays as numpy arrays."""
     L = lib()
-    if _dt(dtype) == FP64:
+    if _dt(dtype) in (FP64, FP64_FMA):
         dx, dy, _ = derive(xmin, xmax, ymin, ymax, W, H, R, "fp64")
         cx = np.array([L.oracle_cx_f64(xmin, dx, j) for j in range(W)], dtype=np.float64)
         cy = np.array([L.oracle_cy_f64(ymax, dy, i) for i in range(H)], dtype=np.float64)

@@ -10,7 +10,7 @@
  *
  * Build (see __graft_entry__.build and tests/conftest.py):
  *   gcc -std=c11 -O2 -ffp-contract=off -fno-fast-math -fPIC -shared \
- *       -o oracle/liboracle.so oracle/oracle.c
+ *       -o oracle/liboracle.so oracle/oracle.c -lm
  * -ffp-contract=off forbids fusing a*b+c into one FMA; on x86-64 all float and
  * double arithmetic is SSE (FLT_EVAL_METHOD == 0), so every operation below is
  * one IEEE-754 round-to-nearest-even operation in its own type.
@@ -33,11 +33,13 @@
  * configured grids, mirror symmetry, power-of-two decimation, iterMax
  * monotonicity, and an independent numpy re-implementation.
  */
+#include <math.h>
 #include <stdint.h>
 #include <stddef.h>
 
 #define ORACLE_FP64 0
 #define ORACLE_FP32 1
+#define ORACLE_FP64_FMA 2
 
 /* ---------------------------------------------------------------------------
  * Eq. 1 + Eq. 2 for one point c = cr + i*ci, in double.
@@ -90,6 +92,32 @@ uint32_t oracle_escape_f32(float cr, float ci, uint32_t iterMax, float R2)
 }
 
 /* ---------------------------------------------------------------------------
+ * The fused-multiply-add variant of the same recurrence (reading R17):
+ *   y' = fma(x + x, y, ci);  x' = fma(x, x, -y^2) + cr;  y2' = y' * y';
+ *   |z'|^2 = fma(x', x', y2')
+ * C99 fma() is one correctly rounded fused multiply-add (ISO C 7.12.13.1).
+ * ------------------------------------------------------------------------- */
+uint32_t oracle_escape_f64fma(double cr, double ci, uint32_t iterMax, double R2)
+{
+    double x = 0.0, y = 0.0, y2 = 0.0;
+    uint32_t n = 0;
+    while (n < iterMax) {
+        double two_x = x + x;
+        double new_y = fma(two_x, y, ci);     /* 2xy + ci, one rounding        */
+        double d = fma(x, x, -y2);            /* x^2 - y^2, one rounding       */
+        double new_x = d + cr;
+        x = new_x;
+        y = new_y;
+        y2 = y * y;
+        n = n + 1;
+        double mag2 = fma(x, x, y2);          /* x^2 + y^2, one rounding       */
+        if (mag2 > R2)
+            break;
+    }
+    return n;
+}
+
+/* ---------------------------------------------------------------------------
  * Step a1: derived constants.  dx = (xmax - xmin)/W, dy = (ymax - ymin)/H,
  * R2 = R*R, each one IEEE operation.  out = {dx, dy, R2}.
  * ------------------------------------------------------------------------- */
@@ -135,14 +163,16 @@ int oracle_render_rows(double xmin, double xmax, double ymin, double ymax,
 {
     if (W == 0 || H == 0 || iterMax == 0 || row0 > row1 || row1 > H || out == NULL)
         return -1;
-    if (dtype == ORACLE_FP64) {
+    if (dtype == ORACLE_FP64 || dtype == ORACLE_FP64_FMA) {
         double k[3];
         oracle_derive_f64(xmin, xmax, ymin, ymax, W, H, R, k);
         for (uint32_t i = row0; i < row1; ++i) {
             double ci = oracle_cy_f64(ymax, k[1], i);
             for (uint32_t j = 0; j < W; ++j) {
                 double cr = oracle_cx_f64(xmin, k[0], j);
-                out[(size_t)(i - row0) * W + j] = oracle_escape_f64(cr, ci, iterMax, k[2]);
+                out[(size_t)(i - row0) * W + j] = dtype == ORACLE_FP64
+                    ? oracle_escape_f64(cr, ci, iterMax, k[2])
+                    : oracle_escape_f64fma(cr, ci, iterMax, k[2]);
             }
         }
         return 0;
@@ -174,12 +204,14 @@ int oracle_render_pixels(double xmin, double xmax, double ymin, double ymax,
     for (size_t p = 0; p < n; ++p)
         if (ii[p] >= H || jj[p] >= W)
             return -1;
-    if (dtype == ORACLE_FP64) {
+    if (dtype == ORACLE_FP64 || dtype == ORACLE_FP64_FMA) {
         double k[3];
         oracle_derive_f64(xmin, xmax, ymin, ymax, W, H, R, k);
-        for (size_t p = 0; p < n; ++p)
-            out[p] = oracle_escape_f64(oracle_cx_f64(xmin, k[0], jj[p]),
-                                       oracle_cy_f64(ymax, k[1], ii[p]), iterMax, k[2]);
+        for (size_t p = 0; p < n; ++p) {
+            double cr = oracle_cx_f64(xmin, k[0], jj[p]), ci = oracle_cy_f64(ymax, k[1], ii[p]);
+            out[p] = dtype == ORACLE_FP64 ? oracle_escape_f64(cr, ci, iterMax, k[2])
+                                          : oracle_escape_f64fma(cr, ci, iterMax, k[2]);
+        }
         return 0;
     }
     if (dtype == ORACLE_FP32) {

@@ -57,13 +57,14 @@ int derive(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint3
     if (W == 0 || H == 0) return fail(MANDEL_EINVAL, "W and H must be >= 1");
     if ((uint64_t)W * (uint64_t)H > (uint64_t)(SIZE_MAX / 4)) return fail(MANDEL_EINVAL, "W*H*4 overflows size_t");
     if (iter_max == 0) return fail(MANDEL_EINVAL, "iterMax must be >= 1");
-    if (dtype != MANDEL_FP64 && dtype != MANDEL_FP32) return fail(MANDEL_EINVAL, "dtype out of range");
+    if (dtype != MANDEL_FP64 && dtype != MANDEL_FP32 && dtype != MANDEL_FP64_FMA)
+        return fail(MANDEL_EINVAL, "dtype out of range");
     if (!std::isfinite(xmin) || !std::isfinite(xmax) || !std::isfinite(ymin) || !std::isfinite(ymax))
         return fail(MANDEL_EINVAL, "window bounds must be finite");
     if (!(xmin < xmax) || !(ymin < ymax)) return fail(MANDEL_EINVAL, "need xmin < xmax and ymin < ymax");
     if (!std::isfinite(R) || !(R > 0.0)) return fail(MANDEL_EINVAL, "R must be finite and > 0");
     std::memset(&d, 0, sizeof(d));
-    if (dtype == MANDEL_FP64) {
+    if (dtype == MANDEL_FP64 || dtype == MANDEL_FP64_FMA) {
         volatile double r2 = R * R;
         if (!std::isfinite((double)r2) || !(r2 > 0.0)) return fail(MANDEL_EINVAL, "R*R not finite/positive in fp64");
         volatile double dx = (xmax - xmin) / (double)W;
@@ -147,7 +148,7 @@ int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
 struct DeviceCtx {
     bool init = false;
     int sms = 0;
-    int occ_cache[2][5][5][5] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
+    int occ_cache[3][5][5][5] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
     bool peer_to0 = false;
 };
 
@@ -198,24 +199,27 @@ int minb_index(int v) {
 #define MANDEL_MINB_ROW(K, T, I) \
     {K<T, I, 1>, K<T, I, 4>, K<T, I, 5>, K<T, I, 6>, K<T, I, 8>}
 
-// kernel_fn(fp32, variant, ilp, minb index); nullptr if not instantiated.
+// kernel_fn(dtype, variant, ilp, minb index); nullptr if not instantiated.
+// dtype index: 0 = MANDEL_FP64, 1 = MANDEL_FP32, 2 = MANDEL_FP64_FMA.
+#define MANDEL_ILP4_ROWS(K, A)                                                              \
+    {MANDEL_MINB_ROW(K, A, 1), MANDEL_MINB_ROW(K, A, 2), MANDEL_MINB_ROW(K, A, 3),        \
+     MANDEL_MINB_ROW(K, A, 4)}
+#define MANDEL_ILP2_ROWS(K, A) {MANDEL_MINB_ROW(K, A, 1), MANDEL_MINB_ROW(K, A, 2)}
 KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
     using namespace mandel;
-    static const KernelFn eager[2][4][5] = {
-        {MANDEL_MINB_ROW(escape_refill_kernel, double, 1), MANDEL_MINB_ROW(escape_refill_kernel, double, 2),
-         MANDEL_MINB_ROW(escape_refill_kernel, double, 3), MANDEL_MINB_ROW(escape_refill_kernel, double, 4)},
-        {MANDEL_MINB_ROW(escape_refill_kernel, float, 1), MANDEL_MINB_ROW(escape_refill_kernel, float, 2),
-         MANDEL_MINB_ROW(escape_refill_kernel, float, 3), MANDEL_MINB_ROW(escape_refill_kernel, float, 4)},
-    };
-    static const KernelFn lazy[2][2][5] = {
-        {MANDEL_MINB_ROW(escape_lazy_kernel, double, 1), MANDEL_MINB_ROW(escape_lazy_kernel, double, 2)},
-        {MANDEL_MINB_ROW(escape_lazy_kernel, float, 1), MANDEL_MINB_ROW(escape_lazy_kernel, float, 2)},
-    };
-    static const KernelFn adaptive[2][2][5] = {
-        {MANDEL_MINB_ROW(escape_adaptive_kernel, double, 1), MANDEL_MINB_ROW(escape_adaptive_kernel, double, 2)},
-        {MANDEL_MINB_ROW(escape_adaptive_kernel, float, 1), MANDEL_MINB_ROW(escape_adaptive_kernel, float, 2)},
-    };
-    if (variant == MANDEL_KERNEL_STATIC) return fp32 ? escape_static_kernel<float> : escape_static_kernel<double>;
+    static const KernelFn eager[3][4][5] = {MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF64),
+                                            MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF32),
+                                            MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF64Fma)};
+    static const KernelFn lazy[3][2][5] = {MANDEL_ILP2_ROWS(escape_lazy_kernel, ArithF64),
+                                           MANDEL_ILP2_ROWS(escape_lazy_kernel, ArithF32),
+                                           MANDEL_ILP2_ROWS(escape_lazy_kernel, ArithF64Fma)};
+    static const KernelFn adaptive[3][2][5] = {MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF64),
+                                               MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF32),
+                                               MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF64Fma)};
+    static const KernelFn statics[3] = {escape_static_kernel<ArithF64>, escape_static_kernel<ArithF32>,
+                                        escape_static_kernel<ArithF64Fma>};
+    if (fp32 < 0 || fp32 > 2) return nullptr;
+    if (variant == MANDEL_KERNEL_STATIC) return statics[fp32];
     if (mi < 0 || mi > 4) return nullptr;
     if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
     if (variant == MANDEL_KERNEL_LAZY && ilp >= 1 && ilp <= 2) return lazy[fp32][ilp - 1][mi];
@@ -227,8 +231,9 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
 struct KernelChoice {
     int variant, ilp, minb;
 };
-constexpr KernelChoice kDefaultChoice[2] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp64: C2 75.6%, C5 84.4%
-                                            {MANDEL_KERNEL_EAGER, 4, 1}};  // fp32: C3 53.8% (issue-bound)
+constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp64: C2 75.6%, C5 84.4%
+                                            {MANDEL_KERNEL_EAGER, 4, 1},   // fp32: C3 53.8% (issue-bound)
+                                            {MANDEL_KERNEL_EAGER, 2, 1}};  // fp64 FMA
 constexpr uint32_t kDefaultRefillLanes = 8;
 constexpr uint32_t kDefaultAdaptLo = 16, kDefaultAdaptHi = 64;
 constexpr int kDefaultBands = 8;  // C2: 4 -> 8.50 ms, 8 -> 8.29 ms, 16 -> 8.86 ms per render (e2e_probe)  // pipelined device->host hand-off (one GPU, host output)
@@ -365,7 +370,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.xminf = d.xminf; p.ymaxf = d.ymaxf; p.dxf = d.dxf; p.dyf = d.dyf;
     p.r2bits = d.r2bits;
     // candidate key threshold: fp64 -> high word of bits(R2)+1; fp32 -> bits(R2)+1 (exact)
-    p.r2cand = dtype == MANDEL_FP64 ? (int)(((unsigned long long)d.r2bits + 1ull) >> 32)
+    p.r2cand = dtype != MANDEL_FP32 ? (int)(((unsigned long long)d.r2bits + 1ull) >> 32)
                                     : (int)(d.r2bits + 1);
     p.W = W; p.H = H; p.iter_max = iter_max;
     p.scheme = (uint32_t)kscheme;
@@ -388,7 +393,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.fcfs_ctr = fcfs_ctr;
     p.fcfs_sys = fcfs_sys ? 1u : 0u;
     const DeviceCtx& dc = g_dev[device];
-    const int fi = dtype == MANDEL_FP32 ? 1 : 0;
+    const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
     KernelChoice kc = kDefaultChoice[fi];
     if (kernel != MANDEL_KERNEL_REFILL) {
         kc.variant = kernel;

@@ -60,8 +60,11 @@ struct Params {
     uint32_t* fcfs_ctr;              // shared global chunk counter (GPU 0's memory)
 };
 
-template <typename T> struct Arith;
-template <> struct Arith<double> {
+// Arithmetic policies: the storage type T, its RN operations, the escape-test bit
+// pattern, and one z-update in the oracle's exact operation order (step) with its
+// |z|^2 (sumsq).  The kernels are templated on the policy.
+struct ArithF64 {
+    typedef double T;
     typedef long long bits_t;
     static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
     static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
@@ -75,8 +78,38 @@ template <> struct Arith<double> {
     static __device__ __forceinline__ double ymax(const Params& p) { return p.ymax; }
     static __device__ __forceinline__ double dx(const Params& p) { return p.dx; }
     static __device__ __forceinline__ double dy(const Params& p) { return p.dy; }
+    // Eq. 1: y' = (x + x) y + ci;  x' = (x2 - y2) + cr;  x2 = x'x';  y2 = y'y'  (8 ops with sumsq)
+    static __device__ __forceinline__ void step(double& x, double& y, double& x2, double& y2,
+                                                double cr, double ci) {
+        const double ny = add(mul(add(x, x), y), ci);
+        const double nx = add(sub(x2, y2), cr);
+        x = nx;
+        y = ny;
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
+    static __device__ __forceinline__ double sumsq(double, double, double x2, double y2) { return add(x2, y2); }
 };
-template <> struct Arith<float> {
+
+// MANDEL_FP64_FMA: the same recurrence with fused multiply-adds (R17):
+//   y' = fma(x + x, y, ci);  x' = fma(x, x, -y2) + cr;  y2 = y'y';  |z|^2 = fma(x', x', y2)
+// -- 6 FP64 instructions per iteration instead of 8; a different map (own oracle).
+struct ArithF64Fma : ArithF64 {
+    static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+    static __device__ __forceinline__ void step(double& x, double& y, double& x2, double& y2,
+                                                double cr, double ci) {
+        const double ny = fma(add(x, x), y, ci);
+        const double nx = add(fma(x, x, -y2), cr);
+        x = nx;
+        y = ny;
+        y2 = mul(y, y);
+        x2 = 0.0;  // not carried (dead)
+    }
+    static __device__ __forceinline__ double sumsq(double x, double, double, double y2) { return fma(x, x, y2); }
+};
+
+struct ArithF32 {
+    typedef float T;
     typedef int bits_t;
     static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
     static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
@@ -88,30 +121,29 @@ template <> struct Arith<float> {
     static __device__ __forceinline__ float ymax(const Params& p) { return p.ymaxf; }
     static __device__ __forceinline__ float dx(const Params& p) { return p.dxf; }
     static __device__ __forceinline__ float dy(const Params& p) { return p.dyf; }
+    static __device__ __forceinline__ void step(float& x, float& y, float& x2, float& y2, float cr, float ci) {
+        const float ny = add(mul(add(x, x), y), ci);
+        const float nx = add(sub(x2, y2), cr);
+        x = nx;
+        y = ny;
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
+    static __device__ __forceinline__ float sumsq(float, float, float x2, float y2) { return add(x2, y2); }
 };
 
 // One z-update of Eq. 1 and the Eq. 2 escape test, in the oracle's operation order.
 #define MANDEL_STEP()                                              \
     do {                                                           \
-        T ny_ = A::add(A::mul(A::add(x, x), y), ci);               \
-        T nx_ = A::add(A::sub(x2, y2), cr);                        \
-        x = nx_;                                                   \
-        y = ny_;                                                   \
-        x2 = A::mul(x, x);                                         \
-        y2 = A::mul(y, y);                                         \
-        esc = A::bits(A::add(x2, y2)) > r2;                        \
+        A::step(x, y, x2, y2, cr, ci);                             \
+        esc = A::bits(A::sumsq(x, y, x2, y2)) > r2;                \
     } while (0)
 
 // The same update on slot s of the per-lane arrays (refill kernel).
 #define MANDEL_STEP_SLOT(s)                                                \
     do {                                                                   \
-        T ny_ = A::add(A::mul(A::add(x[s], x[s]), y[s]), ci[s]);           \
-        T nx_ = A::add(A::sub(x2[s], y2[s]), cr[s]);                       \
-        x[s] = nx_;                                                        \
-        y[s] = ny_;                                                        \
-        x2[s] = A::mul(x[s], x[s]);                                        \
-        y2[s] = A::mul(y[s], y[s]);                                        \
-        esc[s] = A::key(A::add(x2[s], y2[s])) >= r2c;                      \
+        A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);                   \
+        esc[s] = A::key(A::sumsq(x[s], y[s], x2[s], y2[s])) >= r2c;        \
     } while (0)
 
 // chunk_map is private to one rank's kernel (its own HBM): device-scope relaxed
@@ -222,10 +254,11 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
 // tile stream, so lanes stay busy through the divergence near the set boundary.
 // Per-slot state: z (x, y), x2, y2, c (cr, ci), remaining iterations, output ptr.
 // ---------------------------------------------------------------------------
-template <typename T, int ILP, int MINB>
+template <typename AR, int ILP, int MINB>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
-    typedef Arith<T> A;
+    typedef AR A;
+    typedef typename AR::T T;
     typedef typename A::bits_t B;
     const unsigned FULL = 0xffffffffu;
     const uint32_t lane = threadIdx.x & 31;
@@ -353,7 +386,7 @@ escape_refill_kernel(const Params p) {
             for (int s = 0; s < ILP; ++s) {
                 // exact Eq. 2 test on the candidate's own |z|^2 (same operands, same bits);
                 // idle slots hold z = 0 and never pass it
-                fin[s] = A::bits(A::add(x2[s], y2[s])) > r2;
+                fin[s] = A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2;
                 any_fin |= fin[s];
             }
             if (k == kmax || __any_sync(FULL, any_fin)) break;
@@ -395,24 +428,19 @@ escape_refill_kernel(const Params p) {
 // (n counts the escaping update too, reading R3), then clear `lv` on escape.
 #define LAZY_STEP_SLOT(s)                                                  \
     do {                                                                   \
-        T ny_ = A::add(A::mul(A::add(x[s], x[s]), y[s]), ci[s]);           \
-        T nx_ = A::add(A::sub(x2[s], y2[s]), cr[s]);                       \
-        x[s] = nx_;                                                        \
-        y[s] = ny_;                                                        \
-        x2[s] = A::mul(x[s], x[s]);                                        \
-        y2[s] = A::mul(y[s], y[s]);                                        \
-        const bool in_ = !(A::bits(A::add(x2[s], y2[s])) > r2);           \
+        A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);                   \
+        const bool in_ = !(A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2); \
         n[s] += lv[s];                                                     \
         lv[s] = in_ ? lv[s] : 0u;                                          \
     } while (0)
 
-template <typename T, int ILP, bool DRAIN>
+template <typename AR, int ILP, bool DRAIN, typename T = typename AR::T>
 __device__ __forceinline__ void lazy_run(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
                                          const T (&cr)[ILP], const T (&ci)[ILP],
                                          uint32_t (&n)[ILP], uint32_t (&lv)[ILP],
-                                         typename Arith<T>::bits_t r2, uint32_t kmax,
+                                         typename AR::bits_t r2, uint32_t kmax,
                                          int max_live_full) {
-    typedef Arith<T> A;
+    typedef AR A;
     const unsigned FULL = 0xffffffffu;
     uint32_t k = 0;
     for (;;) {
@@ -435,10 +463,11 @@ __device__ __forceinline__ void lazy_run(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP],
     }
 }
 
-template <typename T, int ILP, int MINB>
+template <typename AR, int ILP, int MINB>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_lazy_kernel(const Params p) {
-    typedef Arith<T> A;
+    typedef AR A;
+    typedef typename AR::T T;
     typedef typename A::bits_t B;
     const unsigned FULL = 0xffffffffu;
     const uint32_t lane = threadIdx.x & 31;
@@ -519,8 +548,8 @@ escape_lazy_kernel(const Params p) {
         }
         if (!__any_sync(FULL, any_live)) break;
         const uint32_t kmax = __reduce_min_sync(FULL, left);
-        if (more) lazy_run<T, ILP, false>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, max_live_full);
-        else lazy_run<T, ILP, true>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, 0);
+        if (more) lazy_run<AR, ILP, false>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, max_live_full);
+        else lazy_run<AR, ILP, true>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, 0);
 
         // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)
 #pragma unroll
@@ -552,21 +581,17 @@ escape_lazy_kernel(const Params p) {
 // ---------------------------------------------------------------------------
 #define ADAPT_LAZY_STEP_SLOT(s)                                            \
     do {                                                                   \
-        T ny_ = A::add(A::mul(A::add(x[s], x[s]), y[s]), ci[s]);           \
-        T nx_ = A::add(A::sub(x2[s], y2[s]), cr[s]);                       \
-        x[s] = nx_;                                                        \
-        y[s] = ny_;                                                        \
-        x2[s] = A::mul(x[s], x[s]);                                        \
-        y2[s] = A::mul(y[s], y[s]);                                        \
-        const bool in_ = !(A::bits(A::add(x2[s], y2[s])) > r2);           \
+        A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);                   \
+        const bool in_ = !(A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2); \
         rem[s] -= lv[s];                                                   \
         lv[s] = in_ ? lv[s] : 0u;                                          \
     } while (0)
 
-template <typename T, int ILP, int MINB>
+template <typename AR, int ILP, int MINB>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_adaptive_kernel(const Params p) {
-    typedef Arith<T> A;
+    typedef AR A;
+    typedef typename AR::T T;
     typedef typename A::bits_t B;
     const unsigned FULL = 0xffffffffu;
     const uint32_t lane = threadIdx.x & 31;
@@ -689,7 +714,7 @@ escape_adaptive_kernel(const Params p) {
                 bool any_fin = false;
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
-                    fin[s] = A::bits(A::add(x2[s], y2[s])) > r2;
+                    fin[s] = A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2;
                     any_fin |= fin[s];
                 }
                 if (k == kmax || __any_sync(FULL, any_fin)) break;
@@ -751,10 +776,11 @@ escape_adaptive_kernel(const Params p) {
 // one warp = 32 consecutive pixels of a row), plain per-lane early exit.
 // Static schemes only.  Kept for A/B measurement of the refill design.
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename AR>
 __global__ void __launch_bounds__(kCtaThreads)
 escape_static_kernel(const Params p) {
-    typedef Arith<T> A;
+    typedef AR A;
+    typedef typename AR::T T;
     typedef typename A::bits_t B;
     const B r2 = (B)p.r2bits;
     const uint32_t j = blockIdx.x * 32 + threadIdx.x;

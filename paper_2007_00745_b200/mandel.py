@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmandel.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "mandel.h")
 
-MANDEL_FP64, MANDEL_FP32 = 0, 1
+MANDEL_FP64, MANDEL_FP32, MANDEL_FP64_FMA = 0, 1, 2
 MANDEL_BLOCK, MANDEL_CYCLIC, MANDEL_FCFS, MANDEL_FCFS_MASTER = 0, 1, 2, 3
 MANDEL_OK, MANDEL_EINVAL, MANDEL_ENODEV, MANDEL_ENOMEM = 0, -1, -2, -3
 MANDEL_ECUDA, MANDEL_ECOMM, MANDEL_EBUSY, MANDEL_EIO = -4, -5, -6, -7
@@ -34,7 +34,7 @@ KERNELS = {"refill": (0, 0), "static": (1, 0), "eager": (2, 0), "lazy": (3, 0),
 MANDEL_MAX_GPUS = 64
 MANDEL_IPC_HANDLE_BYTES = 64
 
-DTYPES = {"fp64": MANDEL_FP64, "fp32": MANDEL_FP32}
+DTYPES = {"fp64": MANDEL_FP64, "fp32": MANDEL_FP32, "fp64fma": MANDEL_FP64_FMA}
 SCHEMES = {"block": MANDEL_BLOCK, "naive": MANDEL_BLOCK, "cyclic": MANDEL_CYCLIC,
            "alternating": MANDEL_CYCLIC, "fcfs": MANDEL_FCFS, "fcfs_master": MANDEL_FCFS_MASTER}
 

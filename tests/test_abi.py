@@ -30,9 +30,16 @@ def test_library_is_sm100a_only(mandel):
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", mandel.LIB_PATH], capture_output=True,
                           text=True).stdout
-    # no FMA contraction anywhere in the escape kernels (bit-exactness, R10)
+    # no FMA contraction in any kernel except the explicit FMA dtype's (R10, R17)
+    fn, fma_fns = None, 0
     for line in sass.splitlines():
-        assert "DFMA" not in line and "FFMA" not in line, line
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+            continue
+        if "DFMA" in line or "FFMA" in line:
+            assert fn and "ArithF64Fma" in fn, (fn, line)
+            fma_fns += 1
+    assert fma_fns > 0
 
 
 def test_abi_version_and_strerror(mandel):
@@ -54,7 +61,7 @@ def _call(mandel, **kw):
 BAD_ARGS = [
     dict(W=0), dict(H=0), dict(iter_max=0), dict(R=0.0), dict(R=-1.0), dict(R=math.inf),
     dict(R=1e200), dict(xmin=math.nan), dict(ymax=math.inf), dict(xmin=1.5), dict(ymin=2.0),
-    dict(dtype=2), dict(dtype=-1), dict(scheme=4), dict(scheme=3, ngpus=1), dict(H=3, ngpus=4),
+    dict(dtype=3), dict(dtype=-1), dict(dtype=2, R=1e200), dict(scheme=4), dict(scheme=3, ngpus=1), dict(H=3, ngpus=4),
     dict(dtype=1, R=1e20), dict(dtype=1, xmin=-1e39), dict(dtype=1, xmin=1.0, xmax=1.0 + 1e-12),
     dict(W=0xFFFFFFFF, H=0xFFFFFFFF) if ctypes.sizeof(ctypes.c_size_t) == 4 else dict(W=0),
 ]

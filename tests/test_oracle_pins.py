@@ -247,3 +247,53 @@ def test_fp32_differs_from_fp64(oracle):
     a = oracle.render(wl.C1)
     b = oracle.render(wl.C1.with_(dtype="fp32"))
     assert 0 < int((a != b).sum()) < 5000
+
+
+# --------------------------------------------------------------------------
+# The FMA dtype (R17): its own oracle, pinned independently
+# --------------------------------------------------------------------------
+def _fma(a: float, b: float, c: float) -> float:
+    """Correctly rounded fused multiply-add from exact rationals (CPython's
+    Fraction -> float conversion rounds to nearest, ties to even)."""
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def _py_fma_escape(cr, ci, iter_max, r2):
+    x = y = y2 = 0.0
+    n = 0
+    while n < iter_max:
+        ny = _fma(x + x, y, ci)
+        nx = _fma(x, x, -y2) + cr
+        x, y = nx, ny
+        y2 = y * y
+        n += 1
+        if _fma(x, x, y2) > r2:
+            break
+    return n
+
+
+def test_fma_oracle_pins(oracle):
+    for p in _golden("escape_pins.json")["hand_iterated"]:
+        assert oracle.escape(p["c"][0], p["c"][1], p["iter_max"], p["R"], "fp64fma") == p["count"]
+    g = _golden("escape_pins.json")["never_escape"]
+    for cr, ci in g["points"]:
+        assert oracle.escape(cr, ci, g["iter_max"], g["R"], "fp64fma") == g["iter_max"]
+
+
+def test_fma_oracle_vs_exact_rounding_reference(oracle):
+    for cfg in wl.random_small_configs(12, 100, "fp64fma"):
+        cfg = cfg.with_(W=min(cfg.W, 12), H=min(cfg.H, 12))
+        got = oracle.render(cfg)
+        cx, cy = oracle.axes(*cfg.args()[:4], cfg.W, cfg.H, cfg.R, "fp64")
+        for i in range(cfg.H):
+            for j in range(cfg.W):
+                assert got[i, j] == _py_fma_escape(float(cx[j]), float(cy[i]), cfg.iter_max,
+                                                   cfg.R * cfg.R), (cfg, i, j)
+
+
+def test_fma_map_is_its_own(oracle):
+    # identical on C1, but a different map where rounding matters (C4's zoom window)
+    assert np.array_equal(oracle.render(wl.C1), oracle.render(wl.C1.with_(dtype="fp64fma")))
+    z = wl.C4.with_(W=512, H=512, iter_max=3000)
+    d = int((oracle.render(z) != oracle.render(z.with_(dtype="fp64fma"))).sum())
+    assert 0 < d < 512 * 512 // 20

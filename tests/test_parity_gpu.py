@@ -54,7 +54,7 @@ KERNELS = ["refill", "refill1", "refill2", "refill3", "refill4", "lazy1", "lazy2
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32", "fp64fma"])
 @pytest.mark.parametrize("scheme", SCHEMES)
 @pytest.mark.parametrize("ngpus", [1, 2, 3, 5, 8])
 def test_c1_all_schemes(mandel, oracle, dtype, scheme, ngpus, kernel):
@@ -83,7 +83,7 @@ def test_static_kernel_variant(mandel, oracle, dtype, scheme):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32", "fp64fma"])
 def test_random_small_configs(mandel, oracle, dtype, kernel):
     for k, cfg in enumerate(wl.random_small_configs(50, 0, dtype)):
         want = oracle.render(cfg)
@@ -213,6 +213,16 @@ def test_full_size_sampled(mandel, oracle, name, nrows, kernel):
         a = out[[p[0] for p in pairs]]
         b = out[[p[1] for p in pairs]]
         assert bool((a == b).all())
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kernel", ["refill", "lazy2"])
+def test_zoom_fma_sampled(mandel, oracle, kernel):
+    # the FMA dtype where it differs from fp64 (C4's zoom), full size, sampled rows
+    cfg = wl.C4.with_(dtype="fp64fma")
+    out, st = _render_dev(mandel, cfg, "fcfs", 1, kernel=kernel)
+    _properties(oracle, cfg, out, st)
+    _sampled_rows_check(oracle, cfg, out, 12, seed=17)
 
 
 @pytest.mark.slow
