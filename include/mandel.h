@@ -128,8 +128,8 @@ typedef struct mandel_options {
                                 0 -> library default                                               */
     int      ilp;            /* pixels per lane (EAGER 1..4, LAZY/ADAPTIVE 1..2); 0 -> default     */
     int      min_ctas;       /* register budget as CTAs per SM (1,4,5,6,8); 0 -> default           */
-    int      adapt_lo;       /* ADAPTIVE: eager->lazy below this run length; 0 -> default          */
-    int      adapt_hi;       /* ADAPTIVE: lazy->eager above this run length; 0 -> default          */
+    int      adapt_lo;       /* ADAPTIVE: eager->lazy when the mean eager run is shorter; 0 -> default */
+    int      adapt_hi;       /* ADAPTIVE: lazy runs before probing eager again; 0 -> default         */
     int      bands;          /* one GPU + out_host: row bands whose device->host copies overlap
                                 the later bands' compute (0 -> 8, 1 -> no pipelining, max 32)     */
 } mandel_options;

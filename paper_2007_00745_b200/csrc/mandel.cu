@@ -235,7 +235,7 @@ constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp
                                             {MANDEL_KERNEL_EAGER, 4, 1},   // fp32: C3 53.8% (issue-bound)
                                             {MANDEL_KERNEL_EAGER, 2, 1}};  // fp64 FMA
 constexpr uint32_t kDefaultRefillLanes = 8;
-constexpr uint32_t kDefaultAdaptLo = 16, kDefaultAdaptHi = 64;
+constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
 constexpr int kDefaultBands = 8;  // C2: 4 -> 8.50 ms, 8 -> 8.29 ms, 16 -> 8.86 ms per render (e2e_probe)  // pipelined device->host hand-off (one GPU, host output)
 
 int device_count(int& n) {

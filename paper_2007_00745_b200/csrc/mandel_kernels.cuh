@@ -572,10 +572,10 @@ escape_lazy_kernel(const Params p) {
 // ---------------------------------------------------------------------------
 // K1/K2 (adaptive): the eager kernel's state and exits, plus the lazy kernel's
 // in-loop escape bookkeeping, chosen per warp and per run.  A warp whose eager
-// runs end after fewer than adapt_lo iterations (escapes are dense and
-// incoherent, e.g. C4's zoom) switches to lazy runs, which retire and refill
-// only when refill_lanes lanes hold a finished pixel; a lazy run longer than
-// adapt_hi switches back to eager runs (sparse, coherent escapes: C2, C5).
+// runs average (EMA, weight 1/4) fewer than adapt_lo iterations (escapes are
+// dense and incoherent, e.g. C4's zoom) switches to adapt_hi lazy runs, which
+// retire and refill only when refill_lanes lanes hold a finished pixel, and
+// then probes eager runs again (sparse, coherent escapes: C2, C5).
 // Lazy per-slot bookkeeping: `rem -= lv` and `lv = in ? lv : 0` every iteration
 // with the exact 64-bit Eq. 2 test (rem = iterations still allowed; lv = live).
 // ---------------------------------------------------------------------------
@@ -619,7 +619,9 @@ escape_adaptive_kernel(const Params p) {
     uint32_t* row_ptr = p.out;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
-    bool lazy = false;  // warp-uniform run mode
+    bool lazy = false;           // warp-uniform run mode
+    uint32_t ema = 4 * p.adapt_lo + 64;  // EMA of eager run lengths (x4, fixed point)
+    uint32_t lazy_left = 0;      // lazy runs left before the next eager probe
     unsigned need[ILP];
 #pragma unroll
     for (int s = 0; s < ILP; ++s) need[s] = FULL;
@@ -722,7 +724,11 @@ escape_adaptive_kernel(const Params p) {
 #pragma unroll
             for (int s = 0; s < ILP; ++s)
                 if (rem[s] != kIdleRem) rem[s] -= k;
-            if (k < p.adapt_lo) lazy = true;
+            ema = ema - (ema >> 2) + k;  // ema/4 tracks the eager run length
+            if ((ema >> 2) < p.adapt_lo) {
+                lazy = true;
+                lazy_left = p.adapt_hi;
+            }
         } else {
             // ---- lazy run: per-slot exact bookkeeping, leave when enough lanes are free
             uint32_t lv[ILP];
@@ -749,7 +755,10 @@ escape_adaptive_kernel(const Params p) {
             }
 #pragma unroll
             for (int s = 0; s < ILP; ++s) fin[s] = lv[s] == 0u;  // escaped (or idle)
-            if (k > p.adapt_hi) lazy = false;
+            if (--lazy_left == 0) {
+                lazy = false;            // probe eager again
+                ema = 4 * p.adapt_lo + 16;
+            }
         }
 
         // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)

@@ -26,6 +26,7 @@ from paper_2007_00745_b200 import mandel  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C2")
+    ap.add_argument("--dtype", default=None, help="override the configs' dtype (fp64, fp32, fp64fma)")
     ap.add_argument("--kernels", default="refill1,refill2")
     ap.add_argument("--schemes", default="block,fcfs")
     ap.add_argument("--tiles", default="256")
@@ -40,6 +41,8 @@ def main():
     stream = torch.cuda.current_stream(dev)
     for name in a.configs.split(","):
         cfg = wl.CONFIGS[name]
+        if a.dtype:
+            cfg = cfg.with_(dtype=a.dtype)
         ref = None
         out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
         for kern, scheme, tile, chunk, lanes, minb, adapt in itertools.product(
@@ -76,8 +79,10 @@ def main():
             else:
                 same = bool((ref == out).all())
             giter = st["sum_iters"] / (ms * 1e-3) / 1e9
-            peak = 148 * (64 if cfg.dtype == "fp64" else 128) * 1.965e9 / 8 / 1e9
-            print(json.dumps({"config": name, "kernel": kern, "scheme": scheme, "tile": int(tile),
+            # pixel-iterations/s at the FP pipe peak: 8 ops/iteration (6 for the FMA dtype)
+            ops = 6 if cfg.dtype == "fp64fma" else 8
+            peak = 148 * (128 if cfg.dtype == "fp32" else 64) * 1.965e9 / ops / 1e9
+            print(json.dumps({"config": name, "dtype": cfg.dtype, "kernel": kern, "scheme": scheme, "tile": int(tile),
                               "chunk": int(chunk), "lanes": int(lanes), "minb": int(minb), "adapt": adapt, "ms": round(ms, 4),
                               "kernel_ms": round(sum(ks) / len(ks), 4),
                               "giter_s": round(giter, 2), "frac": round(giter / peak, 4),
