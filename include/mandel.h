@@ -87,7 +87,9 @@ enum mandel_status {
 enum mandel_colour { MANDEL_COLOUR_GRAY = 0, MANDEL_COLOUR_CLASSIC = 1 };
 
 enum mandel_kernel {
-    MANDEL_KERNEL_REFILL = 0,  /* default: the fastest measured configuration for the dtype      */
+    MANDEL_KERNEL_REFILL = 0,  /* default: EAGER, or LAZY when an EAGER render of a strided 1/16
+                                  row sample of the view (once per view, cached) leaves its loop
+                                  more often than once per 10 iterations (incoherent escapes)  */
     MANDEL_KERNEL_STATIC = 1,  /* one pixel per thread, static grid (baseline; BLOCK/CYCLIC only)  */
     MANDEL_KERNEL_EAGER = 2,   /* persistent CTAs, warp tile queue, lane refill on every escape   */
     MANDEL_KERNEL_LAZY = 3,    /* the same, refill batched: escapes recorded in-loop, the warp
@@ -115,6 +117,12 @@ typedef struct mandel_stats {
     uint32_t kernel_launches;      /* kernels this call launched                                    */
     uint32_t ngpus;                /* ranks used                                                    */
     uint32_t ndevices;             /* distinct physical devices used                                */
+    int32_t  kernel_variant;       /* enum mandel_kernel actually run (EAGER/LAZY/ADAPTIVE/STATIC)   */
+    int32_t  kernel_ilp;           /* pixels per lane of that kernel                                */
+    float    probe[2];             /* last view probe (MANDEL_KERNEL_REFILL): eager sample time (ms),
+                                      eager iterations per loop exit (< 10 selects LAZY)           */
+    uint64_t warp_iters;           /* kernel-choice probe only (else 0): loop iterations over warps */
+    uint64_t loop_exits;           /* kernel-choice probe only (else 0): loop exits over warps      */
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
@@ -127,7 +135,7 @@ typedef struct mandel_options {
     int      refill_lanes;   /* LAZY: lanes with a finished pixel that trigger a refill (1..32);
                                 0 -> library default                                               */
     int      ilp;            /* pixels per lane (EAGER 1..4, LAZY/ADAPTIVE 1..2); 0 -> default     */
-    int      min_ctas;       /* register budget as CTAs per SM (1,4,5,6,8); 0 -> default           */
+    int      min_ctas;       /* register budget as CTAs per SM (1,3,4,5,6,8); 0 -> default           */
     int      adapt_lo;       /* ADAPTIVE: eager->lazy when the mean eager run is shorter; 0 -> default */
     int      adapt_hi;       /* ADAPTIVE: lazy runs before probing eager again; 0 -> default         */
     int      bands;          /* one GPU + out_host: row bands whose device->host copies overlap

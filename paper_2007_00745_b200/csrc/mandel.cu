@@ -8,6 +8,7 @@
 //        -Xcompiler -fPIC,-ffp-contract=off -shared -Iinclude -o libmandel.so mandel.cu
 #include <atomic>
 #include <chrono>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -148,7 +149,7 @@ int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
 struct DeviceCtx {
     bool init = false;
     int sms = 0;
-    int occ_cache[3][5][5][5] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
+    int occ_cache[3][5][5][6] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
     bool peer_to0 = false;
 };
 
@@ -187,17 +188,18 @@ struct BusyGuard {
 };
 
 typedef void (*KernelFn)(mandel::Params);
+constexpr int kVariantProbe = 99;  // internal: eager + loop statistics (kernel-choice probe)
 
 // Register-budget instantiations (min CTAs per SM in __launch_bounds__).
-constexpr int kMinbVals[5] = {1, 4, 5, 6, 8};
+constexpr int kMinbVals[6] = {1, 3, 4, 5, 6, 8};
 int minb_index(int v) {
-    for (int i = 0; i < 5; ++i)
+    for (int i = 0; i < 6; ++i)
         if (kMinbVals[i] == v) return i;
     return -1;
 }
 
 #define MANDEL_MINB_ROW(K, T, I) \
-    {K<T, I, 1>, K<T, I, 4>, K<T, I, 5>, K<T, I, 6>, K<T, I, 8>}
+    {K<T, I, 1>, K<T, I, 3>, K<T, I, 4>, K<T, I, 5>, K<T, I, 6>, K<T, I, 8>}
 
 // kernel_fn(dtype, variant, ilp, minb index); nullptr if not instantiated.
 // dtype index: 0 = MANDEL_FP64, 1 = MANDEL_FP32, 2 = MANDEL_FP64_FMA.
@@ -207,20 +209,26 @@ int minb_index(int v) {
 #define MANDEL_ILP2_ROWS(K, A) {MANDEL_MINB_ROW(K, A, 1), MANDEL_MINB_ROW(K, A, 2)}
 KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
     using namespace mandel;
-    static const KernelFn eager[3][4][5] = {MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF64),
+    static const KernelFn eager[3][4][6] = {MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF64),
                                             MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF32),
                                             MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF64Fma)};
-    static const KernelFn lazy[3][2][5] = {MANDEL_ILP2_ROWS(escape_lazy_kernel, ArithF64),
+    static const KernelFn lazy[3][2][6] = {MANDEL_ILP2_ROWS(escape_lazy_kernel, ArithF64),
                                            MANDEL_ILP2_ROWS(escape_lazy_kernel, ArithF32),
                                            MANDEL_ILP2_ROWS(escape_lazy_kernel, ArithF64Fma)};
-    static const KernelFn adaptive[3][2][5] = {MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF64),
+    static const KernelFn adaptive[3][2][6] = {MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF64),
                                                MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF32),
                                                MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF64Fma)};
     static const KernelFn statics[3] = {escape_static_kernel<ArithF64>, escape_static_kernel<ArithF32>,
                                         escape_static_kernel<ArithF64Fma>};
     if (fp32 < 0 || fp32 > 2) return nullptr;
     if (variant == MANDEL_KERNEL_STATIC) return statics[fp32];
-    if (mi < 0 || mi > 4) return nullptr;
+    if (variant == kVariantProbe) {  // the default eager kernels with loop statistics
+        static const KernelFn probe[3] = {escape_refill_kernel<ArithF64, 2, 1, true>,
+                                          escape_refill_kernel<ArithF32, 4, 3, true>,
+                                          escape_refill_kernel<ArithF64Fma, 2, 1, true>};
+        return probe[fp32];
+    }
+    if (mi < 0 || mi > 5) return nullptr;
     if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
     if (variant == MANDEL_KERNEL_LAZY && ilp >= 1 && ilp <= 2) return lazy[fp32][ilp - 1][mi];
     if (variant == MANDEL_KERNEL_ADAPTIVE && ilp >= 1 && ilp <= 2) return adaptive[fp32][ilp - 1][mi];
@@ -231,10 +239,12 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
 struct KernelChoice {
     int variant, ilp, minb;
 };
+// fp32 ILP4 needs min_ctas 3 to stay at 80 registers (3 CTAs of 256 threads per SM);
+// fp64 ILP2 is faster with ptxas' unconstrained schedule (72 registers, also 3 CTAs).
 constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp64: C2 75.6%, C5 84.4%
-                                            {MANDEL_KERNEL_EAGER, 4, 1},   // fp32: C3 53.8% (issue-bound)
+                                            {MANDEL_KERNEL_EAGER, 4, 3},   // fp32: C3 53.9% (issue-bound)
                                             {MANDEL_KERNEL_EAGER, 2, 1}};  // fp64 FMA
-constexpr uint32_t kDefaultRefillLanes = 8;
+constexpr uint32_t kDefaultRefillLanes = 16;  // LAZY on C4: 8 -> 1509, 16 -> 1555 Giter/s
 constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
 constexpr int kDefaultBands = 8;  // C2: 4 -> 8.50 ms, 8 -> 8.29 ms, 16 -> 8.86 ms per render (e2e_probe)  // pipelined device->host hand-off (one GPU, host output)
 
@@ -311,10 +321,19 @@ struct LaunchSpec {
     mandel::Params p;
     dim3 grid, block;
     KernelFn fn;
+    KernelChoice kc;
 };
 
 int occupancy(int device, int fp32, int variant, int ilp, int mi, KernelFn fn, int& occ) {
-    int& c = g_dev[device].occ_cache[fp32][variant][variant == MANDEL_KERNEL_STATIC ? 0 : ilp][mi < 0 ? 0 : mi];
+    const int vi = variant == kVariantProbe ? MANDEL_KERNEL_EAGER : variant;  // same launch shape
+    int& c = g_dev[device].occ_cache[fp32][vi][variant == MANDEL_KERNEL_STATIC ? 0 : ilp][mi < 0 ? 0 : mi];
+    if (variant == kVariantProbe) {
+        CK(cudaSetDevice(device));
+        int cp = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cp, fn, mandel::kCtaThreads, 0));
+        occ = cp > 0 ? cp : 1;
+        return MANDEL_OK;
+    }
     if (c == 0) {
         CK(cudaSetDevice(device));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, fn, mandel::kCtaThreads, 0));
@@ -334,7 +353,7 @@ uint32_t effective_chunk(int scheme, const mandel_options* o) {
 int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
                  size_t state_cap, uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls,
-                 const Plan* band = nullptr) {
+                 const Plan* band = nullptr, const KernelChoice* force = nullptr) {
     // FCFS with a single claimant: the counter hands that rank chunks 0, 1, 2, ... in
     // order, so the dispatch is exactly the one-rank row order; run it as such (no
     // claim atomics or chunk-map lookups; the claim count is reported as ceil(H/chunk)).
@@ -395,7 +414,9 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     const DeviceCtx& dc = g_dev[device];
     const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
     KernelChoice kc = kDefaultChoice[fi];
-    if (kernel != MANDEL_KERNEL_REFILL) {
+    if (force) {
+        kc = *force;
+    } else if (kernel != MANDEL_KERNEL_REFILL) {
         kc.variant = kernel;
         kc.ilp = (o && o->ilp) ? o->ilp : (kernel == MANDEL_KERNEL_LAZY ? 2 : 2);
         kc.minb = (o && o->min_ctas) ? o->min_ctas : 1;
@@ -404,9 +425,10 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         if (o->min_ctas) kc.minb = o->min_ctas;
     }
     const int mi = minb_index(kc.minb);
+    ls.kc = kc;
     ls.fn = kernel_fn(fi, kc.variant, kc.ilp, mi);
     if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
-    const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;
+    const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;  // (the probe variant is persistent)
     int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;
     if (rl < 1 || rl > 32) return fail(MANDEL_EINVAL, "options.refill_lanes must be in 1..32");
     p.refill_lanes = (uint32_t)rl;
@@ -447,13 +469,89 @@ double now_ms() {
     return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
+// ---------------------------------------------------------------------------
+// MANDEL_KERNEL_REFILL chooses, once per view, between the EAGER and LAZY kernels:
+// both render every 16th row (a strided sample of the same image, written to the
+// destination -- the real render rewrites those rows with identical values), the
+// faster one is cached for the view.  Eager wins on smooth views (C2, C5), lazy
+// where neighbouring counts differ (deep zooms, C4).
+// ---------------------------------------------------------------------------
+struct ViewKey {
+    double b[5];
+    uint32_t W, H, it;
+    int dtype;
+    bool operator<(const ViewKey& o) const {
+        if (dtype != o.dtype) return dtype < o.dtype;
+        if (W != o.W) return W < o.W;
+        if (H != o.H) return H < o.H;
+        if (it != o.it) return it < o.it;
+        for (int i = 0; i < 5; ++i)
+            if (b[i] != o.b[i]) return b[i] < o.b[i];
+        return false;
+    }
+};
+std::map<ViewKey, KernelChoice> g_auto;
+float g_probe[2] = {0, 0};  // last probe: eager sample time (ms), eager iterations per exit
+constexpr float kLazyBelowItersPerExit = 10.0f;
+constexpr uint32_t kProbeStride = 16;
+
+int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, uint32_t iter_max,
+                int dtype, const mandel_options* o, uint32_t* image, void* state, size_t state_cap,
+                int device, cudaStream_t s, KernelChoice& out) {
+    const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
+    out = kDefaultChoice[fi];
+    if (o && (o->kernel != MANDEL_KERNEL_REFILL || o->ilp || o->min_ctas > 1)) return MANDEL_OK;
+    if (H < 32 * kProbeStride || (uint64_t)W * H < (1u << 20)) return MANDEL_OK;  // too small to matter
+    ViewKey key{{bounds[0], bounds[1], bounds[2], bounds[3], bounds[4]}, W, H, iter_max, dtype};
+    auto it = g_auto.find(key);
+    if (it != g_auto.end()) {
+        out = it->second;
+        return MANDEL_OK;
+    }
+    const uint32_t n = (H + kProbeStride - 1) / kProbeStride;
+    const Plan pl{n, 0, kProbeStride, n, 0};
+    const KernelChoice cand[2] = {{kVariantProbe, kDefaultChoice[fi].ilp, kDefaultChoice[fi].minb},
+                                  {MANDEL_KERNEL_LAZY, 2, 1}};
+    mandel_options po{};
+    if (o) po = *o;
+    // one eager launch over the sample: its iterations per loop exit measure how
+    // incoherent the escapes are (C2 ~29, C5 ~68, C4's zoom ~3 at ILP2)
+    cudaEvent_t e0, e1;
+    CK(cudaSetDevice(device));
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    LaunchSpec ls;
+    int rc = build_params(d, W, H, iter_max, dtype, MANDEL_BLOCK, 1, 0, &po, image, state, state_cap,
+                          nullptr, false, device, ls, &pl, &cand[0]);
+    if (rc) { cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
+    CK(cudaMemsetAsync(state, 0, state_cap, s));
+    CK(cudaEventRecord(e0, s));
+    rc = launch(ls, s);
+    if (rc) { cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
+    CK(cudaEventRecord(e1, s));
+    mandel::WorkState ws;
+    CK(cudaMemcpyAsync(&ws, state, sizeof(ws), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const float ipe = ws.exits ? (float)((double)ws.warp_iters / (double)ws.exits) : 1e9f;
+    g_probe[0] = ms;
+    g_probe[1] = ipe;
+    out = ipe < kLazyBelowItersPerExit ? cand[1] : kDefaultChoice[fi];
+    g_auto[key] = out;
+    return MANDEL_OK;
+}
+
 // One GPU with a host destination: split the rows into `bands` bands, launch them
 // alternately on two streams (a band's kernel fills the previous band's tail), and
 // copy each finished band to the host on a copy stream while later bands compute --
 // the paper's master file write overlapped with generation.
 int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                   const mandel_options* opts, uint32_t* image, uint32_t* out_host, void* stream0v,
-                  mandel_stats* stats, int bands, size_t sbytes, double t_call) {
+                  mandel_stats* stats, int bands, size_t sbytes, double t_call,
+                  const KernelChoice* choice) {
     int rc = ensure_rank(0, 0, sbytes, nullptr);
     if (rc) return rc;
     CK(cudaSetDevice(0));
@@ -480,7 +578,7 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         Plan pl{nr[b], r0[b], 1, nr[b], 0};
         char* st = reinterpret_cast<char*>(g_root.band_state) + sbytes * b;
         rc = build_params(d, W, H, iter_max, dtype, scheme, 1, 0, opts, image, st, sbytes,
-                          g_root.fcfs_ctr, false, 0, specs[b], &pl);
+                          g_root.fcfs_ctr, false, 0, specs[b], &pl, choice);
         if (rc) return rc;
     }
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
@@ -524,6 +622,8 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
             stats->sum_iters += ws[b].sum_iters;
             stats->pixels += ws[b].pixels;
             stats->rank_rows[0] += ws[b].rows_started;
+            stats->warp_iters += ws[b].warp_iters;
+            stats->loop_exits += ws[b].exits;
         }
         stats->device_ms = kend;
         stats->kernel_ms[0] = kend;
@@ -537,6 +637,10 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         stats->kernel_launches = (uint32_t)bands;
         stats->ngpus = 1;
         stats->ndevices = 1;
+        stats->kernel_variant = specs[0].kc.variant;
+        stats->kernel_ilp = specs[0].kc.ilp;
+        stats->probe[0] = g_probe[0];
+        stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
     }
     return MANDEL_OK;
@@ -589,17 +693,30 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         image = g_root.image;
     }
     const size_t sbytes = state_bytes_for(scheme, H, opts);
+    // kernel choice for this view (MANDEL_KERNEL_REFILL: probed once on device 0)
+    KernelChoice kc;
+    {
+        const double bounds[5] = {xmin, xmax, ymin, ymax, R};
+        rc = ensure_rank(0, 0, sbytes, nullptr);
+        if (rc) return rc;
+        cudaStream_t sp = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
+        rc = auto_choice(d, bounds, W, H, iter_max, dtype, opts, image, g_rank[0].state,
+                         g_rank[0].state_bytes, 0, sp, kc);
+        if (rc) return rc;
+    }
+    const bool auto_k = !opts || opts->kernel == MANDEL_KERNEL_REFILL;
+    const KernelChoice* kcp = auto_k ? &kc : nullptr;
     const int bands = opts && opts->bands ? opts->bands : kDefaultBands;
     if (out_host && ngpus == 1 && bands > 1 && H >= 2 * (uint32_t)bands && scheme != MANDEL_FCFS_MASTER)
         return render_banded(d, W, H, iter_max, dtype, scheme, opts, image, out_host, stream0v,
-                             stats, bands > kMaxBands ? kMaxBands : bands, sbytes, t_call);
+                             stats, bands > kMaxBands ? kMaxBands : bands, sbytes, t_call, kcp);
     std::vector<LaunchSpec> specs(ngpus);
     for (int r = 0; r < ngpus; ++r) {
         const int dev = r % ndev;
         rc = ensure_rank(r, dev, sbytes, nullptr);
         if (rc) return rc;
         rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, g_rank[r].state,
-                          g_rank[r].state_bytes, g_root.fcfs_ctr, nphys > 1, dev, specs[r]);
+                          g_rank[r].state_bytes, g_root.fcfs_ctr, nphys > 1, dev, specs[r], nullptr, kcp);
         if (rc) return rc;
     }
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
@@ -665,6 +782,8 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
             stats->rank_rows[r] = ws[r].rows_started;
             stats->sum_iters += ws[r].sum_iters;
             stats->pixels += ws[r].pixels;
+            stats->warp_iters += ws[r].warp_iters;
+            stats->loop_exits += ws[r].exits;
             claims += ws[r].chunks_claimed;
             if (r != 0) transfers += is_dynamic(scheme) ? ws[r].rows_started : 1u;
             if (scheme == MANDEL_FCFS && ngpus == 1) claims = single_rank_claims(H, opts);
@@ -674,6 +793,10 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         stats->kernel_launches = (uint32_t)launches;
         stats->ngpus = (uint32_t)ngpus;
         stats->ndevices = (uint32_t)nphys;
+        stats->kernel_variant = specs[0].kc.variant;
+        stats->kernel_ilp = specs[0].kc.ilp;
+        stats->probe[0] = g_probe[0];
+        stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
     }
     return MANDEL_OK;
@@ -815,12 +938,18 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->rank_rows[0] = ws.rows_started;
         stats->sum_iters = ws.sum_iters;
         stats->pixels = ws.pixels;
+        stats->warp_iters = ws.warp_iters;
+        stats->loop_exits = ws.exits;
         stats->chunks_claimed = (scheme == MANDEL_FCFS && nranks == 1) ? single_rank_claims(H, opts)
                                                                       : ws.chunks_claimed;
         stats->transfers = rank == 0 ? 0u : (is_dynamic(scheme) ? ws.rows_started : 1u);
         stats->kernel_launches = 1;
         stats->ngpus = 1;
         stats->ndevices = 1;
+        stats->kernel_variant = ls.kc.variant;
+        stats->kernel_ilp = ls.kc.ilp;
+        stats->probe[0] = g_probe[0];
+        stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t0;
     }
     return MANDEL_OK;
@@ -953,6 +1082,7 @@ void mandel_shutdown(void) {
         }
     }
     g_root = Root();
+    g_auto.clear();
     for (auto& d : g_dev) d.init = false;
     cudaGetLastError();
 }

@@ -35,6 +35,8 @@ struct WorkState {
     unsigned int pad0;
     unsigned long long sum_iters; // sum of counts stored by this rank
     unsigned long long pixels;    // pixels stored by this rank
+    unsigned long long warp_iters; // inner-loop iterations summed over warps (eager/adaptive)
+    unsigned long long exits;      // inner-loop exits summed over warps (eager/adaptive)
     // followed by chunk_map[nchunks + 1] (uint32; 0 = unpublished, g+1 = global chunk g,
     // kChunkDone = exhausted)
 };
@@ -231,6 +233,13 @@ __device__ __forceinline__ int draw_tile(const Params& p, uint32_t& row, uint32_
     return kTileOk;
 }
 
+__device__ __forceinline__ void flush_loop_stats(const Params& p, uint32_t witers, uint32_t exits) {
+    if ((threadIdx.x & 31) == 0 && exits) {
+        atomicAdd(&p.ws->warp_iters, (unsigned long long)witers);
+        atomicAdd(&p.ws->exits, (unsigned long long)exits);
+    }
+}
+
 __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long iters,
                                             unsigned long long pix) {
 #pragma unroll
@@ -254,7 +263,9 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
 // tile stream, so lanes stay busy through the divergence near the set boundary.
 // Per-slot state: z (x, y), x2, y2, c (cr, ci), remaining iterations, output ptr.
 // ---------------------------------------------------------------------------
-template <typename AR, int ILP, int MINB>
+// LSTATS: count loop exits and iterations per warp (the kernel-choice probe only:
+// the two counters cost ~3% on C2 in production, measured A/B).
+template <typename AR, int ILP, int MINB, bool LSTATS = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     typedef AR A;
@@ -281,6 +292,7 @@ escape_refill_kernel(const Params p) {
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
+    uint32_t w_iters = 0, w_exits = 0;  // warp-uniform loop statistics (wrap-free below 2^32)
 
     // warp-uniform tile cursor: columns [jcur, jend) of row trow
     uint32_t jcur = 0, jend = 0;
@@ -392,6 +404,11 @@ escape_refill_kernel(const Params p) {
             if (k == kmax || __any_sync(FULL, any_fin)) break;
         }
 
+        if (LSTATS) {
+            w_iters += k;
+            w_exits += 1;
+        }
+
         // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)
 #pragma unroll
         for (int s = 0; s < ILP; ++s) {
@@ -410,6 +427,7 @@ escape_refill_kernel(const Params p) {
         }
     }
     flush_stats(p, my_iters, my_pix);
+    if (LSTATS) flush_loop_stats(p, w_iters, w_exits);
 }
 
 // ---------------------------------------------------------------------------

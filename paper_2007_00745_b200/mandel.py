@@ -15,7 +15,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmandel.so")
+# MANDEL_LIB: an alternative build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("MANDEL_LIB") or os.path.join(_HERE, "libmandel.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "mandel.h")
 
 MANDEL_FP64, MANDEL_FP32, MANDEL_FP64_FMA = 0, 1, 2
@@ -62,6 +63,11 @@ class mandel_stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_uint32),
         ("ngpus", ctypes.c_uint32),
         ("ndevices", ctypes.c_uint32),
+        ("kernel_variant", ctypes.c_int32),
+        ("kernel_ilp", ctypes.c_int32),
+        ("probe", ctypes.c_float * 2),
+        ("warp_iters", ctypes.c_uint64),
+        ("loop_exits", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:
@@ -76,6 +82,10 @@ class mandel_stats(ctypes.Structure):
             "chunks_claimed": int(self.chunks_claimed), "transfers": int(self.transfers),
             "kernel_launches": int(self.kernel_launches), "ngpus": int(self.ngpus),
             "ndevices": int(self.ndevices),
+            "kernel": {0: "refill", 1: "static", 2: "eager", 3: "lazy", 4: "adaptive"}.get(
+                int(self.kernel_variant), str(self.kernel_variant)),
+            "kernel_ilp": int(self.kernel_ilp), "probe": [float(v) for v in self.probe],
+            "warp_iters": int(self.warp_iters), "loop_exits": int(self.loop_exits),
         }
 
 

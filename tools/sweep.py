@@ -86,6 +86,9 @@ def main():
                               "chunk": int(chunk), "lanes": int(lanes), "minb": int(minb), "adapt": adapt, "ms": round(ms, 4),
                               "kernel_ms": round(sum(ks) / len(ks), 4),
                               "giter_s": round(giter, 2), "frac": round(giter / peak, 4),
+                              "ran": f"{st['kernel']}{st['kernel_ilp']}", "probe": st["probe"],
+                              "iters_per_exit": round(st["warp_iters"] / max(st["loop_exits"], 1), 2),
+                              "pix_per_exit": round(st["pixels"] / max(st["loop_exits"], 1), 2),
                               "identical": same}), flush=True)
         del out, ref
         torch.cuda.empty_cache()
