@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 1
+#define MANDEL_ABI_VERSION 2
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -123,6 +123,8 @@ typedef struct mandel_stats {
                                       eager iterations per loop exit (< 10 selects LAZY)           */
     uint64_t warp_iters;           /* kernel-choice probe only (else 0): loop iterations over warps */
     uint64_t loop_exits;           /* kernel-choice probe only (else 0): loop exits over warps      */
+    int32_t  kernel_batch;         /* EAGER: z-updates per escape check actually run (1, 4 or 8)    */
+    int32_t  pad_;
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
@@ -140,6 +142,13 @@ typedef struct mandel_options {
     int      adapt_hi;       /* ADAPTIVE: lazy runs before probing eager again; 0 -> default         */
     int      bands;          /* one GPU + out_host: row bands whose device->host copies overlap
                                 the later bands' compute (0 -> 8, 1 -> no pipelining, max 32)     */
+    int      check_every;    /* EAGER: z-updates per escape test.  1 -> every update (Eq. 2 as
+                                written); 4 or 8 -> batched (R18): |z|^2 is tested after
+                                every 4th/8th update against a threshold just below R^2, and a
+                                batch that crossed it is replayed from its saved start with the
+                                per-update test, so counts are unchanged.  Needs R >= 2 (an
+                                escaped orbit then keeps growing).  0 -> default (4 when valid,
+                                else 1); other values -> MANDEL_EINVAL                              */
 } mandel_options;
 
 /*

@@ -51,6 +51,7 @@ struct Derived {
     double xmin, ymax, dx, dy;
     float xminf, ymaxf, dxf, dyf;
     long long r2bits;
+    bool r2_ge4;  // R2 >= 4 in the working type: the batched escape check is valid (R18)
 };
 
 int derive(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
@@ -78,6 +79,7 @@ int derive(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint3
         d.dy = dy;
         double r2v = r2;
         std::memcpy(&d.r2bits, &r2v, 8);
+        d.r2_ge4 = r2v >= 4.0;
         return MANDEL_OK;
     }
     volatile float xa = (float)xmin, xb = (float)xmax, ya = (float)ymin, yb = (float)ymax, Rf = (float)R;
@@ -100,6 +102,7 @@ int derive(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint3
     int32_t b;
     std::memcpy(&b, &r2v, 4);
     d.r2bits = b;
+    d.r2_ge4 = r2v >= 4.0f;
     return MANDEL_OK;
 }
 
@@ -207,7 +210,11 @@ int minb_index(int v) {
     {MANDEL_MINB_ROW(K, A, 1), MANDEL_MINB_ROW(K, A, 2), MANDEL_MINB_ROW(K, A, 3),        \
      MANDEL_MINB_ROW(K, A, 4)}
 #define MANDEL_ILP2_ROWS(K, A) {MANDEL_MINB_ROW(K, A, 1), MANDEL_MINB_ROW(K, A, 2)}
-KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
+// batched-check EAGER kernels (R18): check every BT z-updates; min CTAs 1 or 3 only
+#define MANDEL_BT_ROW(T, I, BT) {escape_refill_kernel<T, I, 1, BT>, escape_refill_kernel<T, I, 3, BT>}
+#define MANDEL_BT_ROWS(T, BT) \
+    {MANDEL_BT_ROW(T, 1, BT), MANDEL_BT_ROW(T, 2, BT), MANDEL_BT_ROW(T, 3, BT), MANDEL_BT_ROW(T, 4, BT)}
+KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
     using namespace mandel;
     static const KernelFn eager[3][4][6] = {MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF64),
                                             MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF32),
@@ -222,13 +229,27 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
                                         escape_static_kernel<ArithF64Fma>};
     if (fp32 < 0 || fp32 > 2) return nullptr;
     if (variant == MANDEL_KERNEL_STATIC) return statics[fp32];
-    if (variant == kVariantProbe) {  // the default eager kernels with loop statistics
-        static const KernelFn probe[3] = {escape_refill_kernel<ArithF64, 2, 1, true>,
-                                          escape_refill_kernel<ArithF32, 4, 3, true>,
-                                          escape_refill_kernel<ArithF64Fma, 2, 1, true>};
+    if (variant == kVariantProbe) {  // the per-update-check eager kernels with loop statistics
+        static const KernelFn probe[3] = {escape_refill_kernel<ArithF64, 2, 1, 1, true>,
+                                          escape_refill_kernel<ArithF32, 4, 3, 1, true>,
+                                          escape_refill_kernel<ArithF64Fma, 2, 1, 1, true>};
         return probe[fp32];
     }
     if (mi < 0 || mi > 5) return nullptr;
+    if (variant == MANDEL_KERNEL_EAGER && bt > 1) {
+        static const KernelFn b4[3][4][2] = {MANDEL_BT_ROWS(ArithF64, 4), MANDEL_BT_ROWS(ArithF32, 4),
+                                             MANDEL_BT_ROWS(ArithF64Fma, 4)};
+        static const KernelFn b8[3][4][2] = {MANDEL_BT_ROWS(ArithF64, 8), MANDEL_BT_ROWS(ArithF32, 8),
+                                             MANDEL_BT_ROWS(ArithF64Fma, 8)};
+        const int bi = kMinbVals[mi] == 1 ? 0 : (kMinbVals[mi] == 3 ? 1 : -1);
+        if (bi < 0 || ilp < 1 || ilp > 4) return nullptr;
+        static const KernelFn b16[3][4][2] = {MANDEL_BT_ROWS(ArithF64, 16), MANDEL_BT_ROWS(ArithF32, 16),
+                                              MANDEL_BT_ROWS(ArithF64Fma, 16)};
+        if (bt == 4) return b4[fp32][ilp - 1][bi];
+        if (bt == 8) return b8[fp32][ilp - 1][bi];
+        if (bt == 16) return b16[fp32][ilp - 1][bi];
+        return nullptr;
+    }
     if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
     if (variant == MANDEL_KERNEL_LAZY && ilp >= 1 && ilp <= 2) return lazy[fp32][ilp - 1][mi];
     if (variant == MANDEL_KERNEL_ADAPTIVE && ilp >= 1 && ilp <= 2) return adaptive[fp32][ilp - 1][mi];
@@ -238,12 +259,15 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi) {
 // MANDEL_KERNEL_REFILL resolves to these configurations (the measured fastest).
 struct KernelChoice {
     int variant, ilp, minb;
+    int bt;  // EAGER: z-updates per escape check (1 = every update; 4, 8 = batched, R18)
 };
-// fp32 ILP4 needs min_ctas 3 to stay at 80 registers (3 CTAs of 256 threads per SM);
-// fp64 ILP2 is faster with ptxas' unconstrained schedule (72 registers, also 3 CTAs).
-constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 1},   // fp64: C2 75.6%, C5 84.4%
-                                            {MANDEL_KERNEL_EAGER, 4, 3},   // fp32: C3 53.9% (issue-bound)
-                                            {MANDEL_KERNEL_EAGER, 2, 1}};  // fp64 FMA
+// ILP2 runs with ptxas' unconstrained schedule (72 registers, 3 CTAs of 256 threads per SM).
+// Batched escape check with a whole-batch replay on a hit (R18), measured per config
+// (profiles/r01_sweep_batch.jsonl, Giter/s): fp64 C2 check-every-8 ILP2 2061 (per-update
+// check 1722), C5 2360 (1962); fp32 C3 check-every-16 ILP1 3438 (per-update ILP4 2504).
+constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 3, 8},    // fp64
+                                            {MANDEL_KERNEL_EAGER, 1, 3, 16},   // fp32
+                                            {MANDEL_KERNEL_EAGER, 2, 3, 8}};   // fp64 FMA
 constexpr uint32_t kDefaultRefillLanes = 16;  // LAZY on C4: 8 -> 1509, 16 -> 1555 Giter/s
 constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
 constexpr int kDefaultBands = 8;  // C2: 4 -> 8.50 ms, 8 -> 8.29 ms, 16 -> 8.86 ms per render (e2e_probe)  // pipelined device->host hand-off (one GPU, host output)
@@ -391,6 +415,10 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     // candidate key threshold: fp64 -> high word of bits(R2)+1; fp32 -> bits(R2)+1 (exact)
     p.r2cand = dtype != MANDEL_FP32 ? (int)(((unsigned long long)d.r2bits + 1ull) >> 32)
                                     : (int)(d.r2bits + 1);
+    // batched-check threshold (R18): key(R2) lowered by a relative margin far above the
+    // rounding drift of an escaped orbit over 8 updates -- 2^-12 (fp64), 2^-2 (fp32)
+    p.r2batch = dtype != MANDEL_FP32 ? (uint32_t)((unsigned long long)d.r2bits >> 32) - 0x100u
+                                     : (uint32_t)d.r2bits - (1u << 21);
     p.W = W; p.H = H; p.iter_max = iter_max;
     p.scheme = (uint32_t)kscheme;
     p.tile_w = tile;
@@ -418,15 +446,30 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         kc = *force;
     } else if (kernel != MANDEL_KERNEL_REFILL) {
         kc.variant = kernel;
-        kc.ilp = (o && o->ilp) ? o->ilp : (kernel == MANDEL_KERNEL_LAZY ? 2 : 2);
+        kc.ilp = (o && o->ilp) ? o->ilp : 2;
         kc.minb = (o && o->min_ctas) ? o->min_ctas : 1;
+        kc.bt = 1;  // an explicit EAGER checks every update unless check_every says otherwise
     } else if (o && (o->ilp || o->min_ctas)) {
         if (o->ilp) kc.ilp = o->ilp;
         if (o->min_ctas) kc.minb = o->min_ctas;
     }
+    // escape-check batching (R18): EAGER only, valid only when R2 >= 4 in the dtype.
+    // Requested (check_every) -> errors if impossible; defaulted -> falls back to 1.
+    const int ce = o ? o->check_every : 0;
+    if (ce < 0 || (ce > 1 && ce != 4 && ce != 8 && ce != 16))
+        return fail(MANDEL_EINVAL, "options.check_every must be 0, 1, 4, 8 or 16");
+    if (kc.variant != MANDEL_KERNEL_EAGER) {
+        if (ce > 1 && !force) return fail(MANDEL_EINVAL, "check_every > 1 needs the EAGER kernel");
+        kc.bt = 1;
+    } else if (ce) {
+        if (ce > 1 && !d.r2_ge4) return fail(MANDEL_EINVAL, "a batched escape check needs R >= 2");
+        kc.bt = ce;
+    } else if (!d.r2_ge4 || (kc.minb != 1 && kc.minb != 3)) {
+        kc.bt = 1;
+    }
     const int mi = minb_index(kc.minb);
     ls.kc = kc;
-    ls.fn = kernel_fn(fi, kc.variant, kc.ilp, mi);
+    ls.fn = kernel_fn(fi, kc.variant, kc.ilp, mi, kc.bt);
     if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
     const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;  // (the probe variant is persistent)
     int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;
@@ -510,8 +553,8 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
     }
     const uint32_t n = (H + kProbeStride - 1) / kProbeStride;
     const Plan pl{n, 0, kProbeStride, n, 0};
-    const KernelChoice cand[2] = {{kVariantProbe, kDefaultChoice[fi].ilp, kDefaultChoice[fi].minb},
-                                  {MANDEL_KERNEL_LAZY, 2, 1}};
+    const KernelChoice cand[2] = {{kVariantProbe, kDefaultChoice[fi].ilp, kDefaultChoice[fi].minb, 1},
+                                  {MANDEL_KERNEL_LAZY, 2, 1, 1}};
     mandel_options po{};
     if (o) po = *o;
     // one eager launch over the sample: its iterations per loop exit measure how
@@ -639,6 +682,7 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         stats->ndevices = 1;
         stats->kernel_variant = specs[0].kc.variant;
         stats->kernel_ilp = specs[0].kc.ilp;
+        stats->kernel_batch = specs[0].kc.bt;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -795,6 +839,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         stats->ndevices = (uint32_t)nphys;
         stats->kernel_variant = specs[0].kc.variant;
         stats->kernel_ilp = specs[0].kc.ilp;
+        stats->kernel_batch = specs[0].kc.bt;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -948,6 +993,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->ndevices = 1;
         stats->kernel_variant = ls.kc.variant;
         stats->kernel_ilp = ls.kc.ilp;
+        stats->kernel_batch = ls.kc.bt;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t0;

@@ -46,6 +46,7 @@ struct Params {
     float xminf, ymaxf, dxf, dyf;    // fp32 mapping constants
     long long r2bits;                // bit pattern of R2 in the working type
     int r2cand;                      // candidate threshold: key(bits(R2) + 1) (see Arith::key)
+    uint32_t r2batch;                // batched-check threshold on ukey, below key(R2) (R18)
     uint32_t W, H, iter_max;
     uint32_t scheme;
     uint32_t tile_w, tiles_per_row;
@@ -76,6 +77,9 @@ struct ArithF64 {
     // 32-bit escape-candidate key: the high word of the bit pattern.  key(s) >= r2cand
     // (= high word of bits(R2) + 1) is necessary for s > R2; exits verify exactly.
     static __device__ __forceinline__ int key(double v) { return __double2hiint(v); }
+    // unsigned key for the batched check: NaN (either sign) and inf compare above any
+    // finite threshold
+    static __device__ __forceinline__ uint32_t ukey(double v) { return (uint32_t)__double2hiint(v); }
     static __device__ __forceinline__ double xmin(const Params& p) { return p.xmin; }
     static __device__ __forceinline__ double ymax(const Params& p) { return p.ymax; }
     static __device__ __forceinline__ double dx(const Params& p) { return p.dx; }
@@ -91,6 +95,11 @@ struct ArithF64 {
         y2 = mul(y, y);
     }
     static __device__ __forceinline__ double sumsq(double, double, double x2, double y2) { return add(x2, y2); }
+    // the carried squares of a restored z (what step() left next to it)
+    static __device__ __forceinline__ void resq(double x, double y, double& x2, double& y2) {
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
 };
 
 // MANDEL_FP64_FMA: the same recurrence with fused multiply-adds (R17):
@@ -108,6 +117,10 @@ struct ArithF64Fma : ArithF64 {
         x2 = 0.0;  // not carried (dead)
     }
     static __device__ __forceinline__ double sumsq(double x, double, double, double y2) { return fma(x, x, y2); }
+    static __device__ __forceinline__ void resq(double, double y, double& x2, double& y2) {
+        x2 = 0.0;
+        y2 = mul(y, y);
+    }
 };
 
 struct ArithF32 {
@@ -119,6 +132,7 @@ struct ArithF32 {
     static __device__ __forceinline__ int bits(float v) { return __float_as_int(v); }
     static __device__ __forceinline__ float cvt(uint32_t v) { return __uint2float_rn(v); }
     static __device__ __forceinline__ int key(float v) { return __float_as_int(v); }  // exact
+    static __device__ __forceinline__ uint32_t ukey(float v) { return (uint32_t)__float_as_int(v); }
     static __device__ __forceinline__ float xmin(const Params& p) { return p.xminf; }
     static __device__ __forceinline__ float ymax(const Params& p) { return p.ymaxf; }
     static __device__ __forceinline__ float dx(const Params& p) { return p.dxf; }
@@ -132,6 +146,10 @@ struct ArithF32 {
         y2 = mul(y, y);
     }
     static __device__ __forceinline__ float sumsq(float, float, float x2, float y2) { return add(x2, y2); }
+    static __device__ __forceinline__ void resq(float x, float y, float& x2, float& y2) {
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
 };
 
 // One z-update of Eq. 1 and the Eq. 2 escape test, in the oracle's operation order.
@@ -253,6 +271,22 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
     }
 }
 
+// Batched check (BT z-updates, then one |z|^2): true if any lane of the warp has a
+// slot whose final |z|^2 key reaches r2b (below key(R2); R18).
+template <typename A, int ILP, int BT, typename T>
+__device__ __forceinline__ bool batch_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
+                                          const T (&cr)[ILP], const T (&ci)[ILP], uint32_t r2b) {
+#pragma unroll
+    for (int u = 0; u < BT; ++u) {
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int s = 0; s < ILP; ++s) m = max(m, A::ukey(A::sumsq(x[s], y[s], x2[s], y2[s])));
+    return __any_sync(0xffffffffu, m >= r2b);
+}
+
 // ---------------------------------------------------------------------------
 // K1/K2: persistent escape kernel with a per-warp tile queue and lane refill.
 // Each lane holds ILP independent pixels ("slots"); their z-updates are
@@ -265,7 +299,7 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
 // ---------------------------------------------------------------------------
 // LSTATS: count loop exits and iterations per warp (the kernel-choice probe only:
 // the two counters cost ~3% on C2 in production, measured A/B).
-template <typename AR, int ILP, int MINB, bool LSTATS = false>
+template <typename AR, int ILP, int MINB, int BT = 1, bool LSTATS = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     typedef AR A;
@@ -276,6 +310,7 @@ escape_refill_kernel(const Params p) {
     const unsigned lt_mask = (1u << lane) - 1u;
     const B r2 = (B)p.r2bits;
     const int r2c = p.r2cand;
+    const uint32_t r2b = p.r2batch;
     const T xmin = A::xmin(p), ymax = A::ymax(p), dx = A::dx(p), dy = A::dy(p);
     const T zero = T(0);
 
@@ -366,11 +401,77 @@ escape_refill_kernel(const Params p) {
         // ---- iterate: Eq. 1 on every slot until some slot is finished.  The hot loop
         // tests a 32-bit candidate key (one compare per slot); on a candidate the warp
         // leaves the loop and verifies the exact 64-bit test, resuming on a false alarm.
+        // BT > 1 (batched check, R18): BT z-updates per test and |z|^2 only
+        // after the last one, against a threshold below R2 that every slot which escaped
+        // inside the batch still exceeds (|z| grows after an escape when R >= 2); on a
+        // hit the warp restores the batch-start state and replays the batch with the
+        // exact per-update test, so each recorded count is the slot's first escaping
+        // update.  Budget tails shorter than BT run the per-update loop below.
         uint32_t k = 0;
         bool fin[ILP];
+        uint32_t kx[ILP];     // per-slot iterations of this run (differs from k for lazy-replay escapes)
+        bool lazy_exit = false;
         for (;;) {
-            for (;;) {
-                if (kmax - k >= 4) {
+            if (BT > 1) {
+                // only z = (x, y) is saved at the batch start; on a hit A::resq rebuilds
+                // the carried squares from it with the same operations (identical bits),
+                // and the whole batch is replayed with the exact per-update test, each
+                // slot's escaping update recorded in-loop; every slot that escaped in the
+                // batch is then retired at once
+                while (kmax - k >= BT) {
+                    T sx[ILP], sy[ILP];
+                    bool hit;
+                    for (;;) {  // the hot loop: BT updates, one test
+#pragma unroll
+                        for (int s = 0; s < ILP; ++s) {
+                            sx[s] = x[s];
+                            sy[s] = y[s];
+                        }
+                        hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b);
+                        if (hit) break;
+                        k += BT;
+                        if (kmax - k < BT) break;
+                    }
+                    if (!hit) break;
+                    uint32_t ne[ILP], lv[ILP];
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) {
+                        x[s] = sx[s];
+                        y[s] = sy[s];
+                        A::resq(x[s], y[s], x2[s], y2[s]);
+                        lv[s] = rem[s] != kIdleRem ? 1u : 0u;
+                        ne[s] = 0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < BT; ++u) {
+#pragma unroll
+                        for (int s = 0; s < ILP; ++s) {
+                            A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+                            const bool in_ = !(A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2);
+                            ne[s] += lv[s];
+                            lv[s] = in_ ? lv[s] : 0u;
+                        }
+                    }
+                    bool any_esc = false;
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) {
+                        fin[s] = rem[s] != kIdleRem && lv[s] == 0u;
+                        kx[s] = k + ne[s];
+                        any_esc |= fin[s];
+                    }
+                    k += BT;
+                    if (__any_sync(FULL, any_esc)) {
+                        lazy_exit = true;
+                        break;
+                    }
+                    // a false alarm (no slot escaped): keep batching from the batch end
+                }
+                if (lazy_exit) break;
+            }
+            const uint32_t lim = kmax;
+            // per-update test up to the end of the budget (tails shorter than BT, BT = 1)
+            while (k < lim) {
+                if (lim - k >= 4) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         bool e = false;
@@ -381,7 +482,6 @@ escape_refill_kernel(const Params p) {
                         if (__any_sync(FULL, e)) { k += u + 1; goto left_loop; }
                     }
                     k += 4;
-                    if (k == kmax) break;
                 } else {
                     bool e = false;
 #pragma unroll
@@ -389,7 +489,7 @@ escape_refill_kernel(const Params p) {
 #pragma unroll
                     for (int s = 0; s < ILP; ++s) e |= esc[s];
                     k += 1;
-                    if (__any_sync(FULL, e) || k == kmax) break;
+                    if (__any_sync(FULL, e)) break;
                 }
             }
         left_loop:
@@ -403,6 +503,9 @@ escape_refill_kernel(const Params p) {
             }
             if (k == kmax || __any_sync(FULL, any_fin)) break;
         }
+#pragma unroll
+        for (int s = 0; s < ILP; ++s)
+            if (!(lazy_exit && fin[s])) kx[s] = k;
 
         if (LSTATS) {
             w_iters += k;
@@ -414,7 +517,7 @@ escape_refill_kernel(const Params p) {
         for (int s = 0; s < ILP; ++s) {
             bool done = false;
             if (rem[s] != kIdleRem) {
-                rem[s] -= k;
+                rem[s] -= kx[s];
                 done = fin[s] || rem[s] == 0;
             }
             if (done) {

@@ -31,7 +31,11 @@ MANDEL_KERNEL_ADAPTIVE = 4
 KERNELS = {"refill": (0, 0), "static": (1, 0), "eager": (2, 0), "lazy": (3, 0),
            "refill1": (2, 1), "refill2": (2, 2), "refill3": (2, 3), "refill4": (2, 4),
            "lazy1": (3, 1), "lazy2": (3, 2), "adaptive": (4, 0), "adaptive1": (4, 1),
-           "adaptive2": (4, 2)}
+           "adaptive2": (4, 2),
+           # EAGER with the batched escape check (check_every 4 / 8; R18)
+           "batch4x1": (2, 1, 4), "batch4x2": (2, 2, 4), "batch4x4": (2, 4, 4),
+           "batch8x1": (2, 1, 8), "batch8x2": (2, 2, 8), "batch8x3": (2, 3, 8), "batch8x4": (2, 4, 8),
+           "batch16x1": (2, 1, 16), "batch16x2": (2, 2, 16), "batch16x4": (2, 4, 16)}
 MANDEL_MAX_GPUS = 64
 MANDEL_IPC_HANDLE_BYTES = 64
 
@@ -68,6 +72,8 @@ class mandel_stats(ctypes.Structure):
         ("probe", ctypes.c_float * 2),
         ("warp_iters", ctypes.c_uint64),
         ("loop_exits", ctypes.c_uint64),
+        ("kernel_batch", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -86,6 +92,7 @@ class mandel_stats(ctypes.Structure):
                 int(self.kernel_variant), str(self.kernel_variant)),
             "kernel_ilp": int(self.kernel_ilp), "probe": [float(v) for v in self.probe],
             "warp_iters": int(self.warp_iters), "loop_exits": int(self.loop_exits),
+            "kernel_batch": int(self.kernel_batch),
         }
 
 
@@ -101,6 +108,7 @@ class mandel_options(ctypes.Structure):
         ("adapt_lo", ctypes.c_int),
         ("adapt_hi", ctypes.c_int),
         ("bands", ctypes.c_int),
+        ("check_every", ctypes.c_int),
     ]
 
 
@@ -194,18 +202,20 @@ def _ptr(a) -> int | None:
 
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
-          refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0):
+          refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
-        kernel, kilp = KERNELS[kernel]
+        kernel, kilp, *kce = KERNELS[kernel]
         ilp = ilp or kilp
+        check_every = check_every or (kce[0] if kce else 0)
     o.refill_lanes = refill_lanes or 0
     o.ilp = ilp or 0
     o.min_ctas = min_ctas or 0
     o.adapt_lo = adapt_lo or 0
     o.adapt_hi = adapt_hi or 0
     o.bands = bands or 0
+    o.check_every = check_every or 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -236,13 +246,13 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      ngpus=1, *, out_host=None, out_dev0=None, stream0=None, chunk_rows=0,
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
-                     bands=0) -> dict:
+                     bands=0, check_every=0) -> dict:
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict."""
     st = mandel_stats()
     o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
-              adapt_hi, bands)
+              adapt_hi, bands, check_every)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st))
@@ -253,11 +263,12 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
 def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, rank, nranks,
                        out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
                        kernel=MANDEL_KERNEL_REFILL, refill_lanes=0, ilp=0,
-                       min_ctas=0, adapt_lo=0, adapt_hi=0) -> dict:
+                       min_ctas=0, adapt_lo=0, adapt_hi=0, check_every=0) -> dict:
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
     pointers valid in this process (own, or mapped with mandel_ipc_open)."""
     st = mandel_stats()
-    o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas, adapt_lo, adapt_hi)
+    o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas, adapt_lo, adapt_hi,
+              0, check_every)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
                                   _ptr(out_root), _ptr(fcfs_counter), stream, ctypes.byref(st))

@@ -50,7 +50,13 @@ def _assert_same(got, want, label):
 # ---------------------------------------------------------------------------
 # whole maps: C1 and reduced shapes, every scheme, logical rank counts, kernels
 # ---------------------------------------------------------------------------
-KERNELS = ["refill", "refill1", "refill2", "refill3", "refill4", "lazy1", "lazy2", "adaptive1", "adaptive2"]
+KERNELS = ["refill", "refill1", "refill2", "refill3", "refill4", "lazy1", "lazy2", "adaptive1", "adaptive2",
+           "batch4x1", "batch4x2", "batch4x4", "batch8x1", "batch8x2", "batch8x3", "batch8x4",
+           "batch16x1", "batch16x2", "batch16x4"]
+
+
+def _batched(mandel, kernel):
+    return len(mandel.KERNELS[kernel]) > 2 and mandel.KERNELS[kernel][2] > 1
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -91,9 +97,10 @@ def test_random_small_configs(mandel, oracle, dtype, kernel):
         ngpus = [1, 2, 3, 4, 5, 8][k % 6]
         if scheme != "fcfs" and cfg.H < ngpus:
             ngpus = 1
+        ce = 1 if (_batched(mandel, kernel) and cfg.R < 2.0) else 0  # R18 needs R >= 2
         out, st = _render_dev(mandel, cfg, scheme, ngpus, tile_px=[0, 1, 7, 32, 33][k % 5],
                               chunk_rows=[0, 1, 3][k % 3], kernel=kernel,
-                              refill_lanes=[0, 1, 3, 16, 32][k % 5])
+                              refill_lanes=[0, 1, 3, 16, 32][k % 5], check_every=ce)
         _assert_same(_host(out), want, f"{cfg.name}/{dtype}/{scheme}/N={ngpus}")
         assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
 
@@ -116,6 +123,11 @@ EDGE = [
 @pytest.mark.parametrize("cfg", EDGE, ids=[c.name for c in EDGE])
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_edge_cases(mandel, oracle, cfg, scheme, kernel):
+    if _batched(mandel, kernel) and cfg.R < 2.0:
+        # the batched check is only valid for R >= 2 (R18): requesting it is an error
+        with pytest.raises(mandel.MandelError):
+            _render_dev(mandel, cfg, scheme, 1, kernel=kernel)
+        return
     want = oracle.render(cfg)
     for ngpus in (1, 4):
         if scheme != "fcfs" and cfg.H < ngpus:
@@ -125,6 +137,47 @@ def test_edge_cases(mandel, oracle, cfg, scheme, kernel):
         _assert_same(got, want, f"{cfg.name}/{scheme}/N={ngpus}")
         assert got.min() >= 1 and got.max() <= cfg.iter_max
         assert st["pixels"] == cfg.pixels
+
+
+# The batched escape check (R18) on the orbits that stress its argument:
+# escapes by a hair (|z|^2 just above R^2, the real axis just left of c = -2 where
+# the escaped orbit grows slowest), orbits that touch |z|^2 = R^2 without escaping
+# (c = -2), escapes that overflow to inf/NaN inside a batch (huge R), and R = 2
+# exactly vs just below 2 (where the library must fall back to the per-update test).
+BATCH_CASES = [
+    wl.Config("left_of_-2", -2.0 - 2e-15, -2.0 + 2e-15, -1e-300, 1e-300, 97, 5, 5000, 2.0, "fp64"),
+    wl.Config("left_of_-2_f32", -2.0000010, -1.9999990, -1e-30, 1e-30, 97, 5, 5000, 2.0, "fp32"),
+    wl.Config("near_-2_row", -2.05, -1.95, -1e-9, 1e-9, 256, 8, 20000, 2.0, "fp64"),
+    wl.Config("hugeR", -2.5, 1.5, -2.0, 2.0, 96, 80, 60, 1e150, "fp64"),
+    wl.Config("hugeR_f32", -2.5, 1.5, -2.0, 2.0, 96, 80, 60, 1e18, "fp32"),
+    wl.Config("R20_seahorse", -0.76, -0.73, 0.09, 0.12, 200, 150, 4000, 20.0, "fp64"),
+    wl.Config("R2_fma", -0.76, -0.73, 0.09, 0.12, 200, 150, 4000, 2.0, "fp64fma"),
+]
+
+
+@pytest.mark.parametrize("kernel", ["refill", "batch4x1", "batch4x2", "batch8x2", "batch8x4",
+                                    "batch16x1", "batch16x2"])
+@pytest.mark.parametrize("cfg", BATCH_CASES, ids=[c.name for c in BATCH_CASES])
+def test_batched_check_adversarial(mandel, oracle, cfg, kernel):
+    want = oracle.render(cfg)
+    for scheme, ngpus in (("fcfs", 1), ("cyclic", 3)):
+        out, st = _render_dev(mandel, cfg, scheme, ngpus, kernel=kernel, tile_px=[0, 16][ngpus % 2])
+        _assert_same(_host(out), want, f"{cfg.name}/{kernel}/{scheme}")
+        assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
+        if kernel != "refill":
+            assert st["kernel_batch"] == mandel.KERNELS[kernel][2]
+
+
+@pytest.mark.parametrize("R,batch", [(2.0, 8), (1.9999999999999998, 1), (1.5, 1), (20.0, 8)])
+def test_batched_check_default_and_fallback(mandel, oracle, R, batch):
+    # default kernel: batched when R >= 2, the per-update test otherwise (same map either way)
+    cfg = wl.C1.with_(W=300, H=200, R=R)
+    out, st = _render_dev(mandel, cfg, "fcfs", 1)
+    _assert_same(_host(out), oracle.render(cfg), f"default R={R}")
+    assert st["kernel_batch"] == batch
+    if batch == 1:
+        with pytest.raises(mandel.MandelError):
+            _render_dev(mandel, cfg, "fcfs", 1, check_every=4)
 
 
 @pytest.mark.parametrize("ngpus", [2, 3, 5, 8])
@@ -198,7 +251,7 @@ def _properties(oracle, cfg, out, st):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("kernel", ["refill", "lazy2"])
+@pytest.mark.parametrize("kernel", ["refill", "lazy2", "refill2", "batch4x2"])
 @pytest.mark.parametrize("name,nrows", [("C2", 48), ("C3", 48), ("C4", 16)])
 def test_full_size_sampled(mandel, oracle, name, nrows, kernel):
     cfg = wl.CONFIGS[name]
