@@ -246,12 +246,23 @@ def run_ours(args):
     peak = fp_peak_tflops(cfg.dtype)
     roof = {"bound": "alu", "unit": "TFLOP/s", "achieved": round(achieved, 4),
             "peak": round(peak, 4), "frac": round(achieved / peak, 4),
-            "traffic": _traffic_from_profiles(cfg, world),
+            "traffic": None,
             "peak_basis": f"{SMS} SMs x {FP64_LANES if cfg.dtype == 'fp64' else FP32_LANES} "
                           f"{cfg.dtype.upper()} lanes x {SM_MAX_MHZ:.0f} MHz (guide unit counts, "
                           "max clock; DESIGN.md Roofline)",
             "kernel_ms": round(kern_ms, 4),
             "ops_per_launch": iters_rank * FLOPS_PER_ITER}
+    prof = _traffic_from_profiles(cfg, world)
+    if prof:
+        # from the committed ncu --set full capture of this kernel (profiles/): DRAM bytes
+        # per launch, and the FP pipe utilisation the kernel actually EXECUTED -- the
+        # batched escape check (R18) executes fewer than 8 FP ops per counted iteration,
+        # so `frac` (counted ops) can exceed the executed pipe utilisation
+        roof["traffic"] = prof.get("dram_bytes_per_launch")
+        pipe = prof.get("fp64_pipe_active_pct" if cfg.dtype != "fp32" else "fma_pipe_active_pct")
+        if pipe is not None:
+            roof["ncu_pipe_active"] = round(pipe / 100.0, 4)
+        roof["ncu_kernel"] = prof.get("kernel")
     if clocks and clocks.get("sm_mhz"):
         roof["frac_at_measured_clock"] = round(achieved / fp_peak_tflops(cfg.dtype, clocks["sm_mhz"]), 4)
 
@@ -365,7 +376,7 @@ def _traffic_from_profiles(cfg, world):
         except (OSError, ValueError):
             continue
         if d.get("config") == cfg.name and d.get("n_gpus", 1) == world:
-            best = d.get("dram_bytes_per_launch")
+            best = d
     return best
 
 

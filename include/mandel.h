@@ -143,12 +143,12 @@ typedef struct mandel_options {
     int      bands;          /* one GPU + out_host: row bands whose device->host copies overlap
                                 the later bands' compute (0 -> 8, 1 -> no pipelining, max 32)     */
     int      check_every;    /* EAGER: z-updates per escape test.  1 -> every update (Eq. 2 as
-                                written); 4 or 8 -> batched (R18): |z|^2 is tested after
-                                every 4th/8th update against a threshold just below R^2, and a
-                                batch that crossed it is replayed from its saved start with the
-                                per-update test, so counts are unchanged.  Needs R >= 2 (an
-                                escaped orbit then keeps growing).  0 -> default (4 when valid,
-                                else 1); other values -> MANDEL_EINVAL                              */
+                                written); 4, 8 or 16 -> batched (R18): |z|^2 is tested
+                                after every 4th/8th/16th update against a threshold just below
+                                R^2; a batch that reaches it is replayed from its saved start
+                                with the exact per-update test, so counts are unchanged.  Needs
+                                R >= 2 (an escaped orbit then keeps growing); fp32 allows <= 8.
+                                0 -> default (8 when valid, else 1); otherwise MANDEL_EINVAL       */
 } mandel_options;
 
 /*

@@ -243,11 +243,10 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
                                              MANDEL_BT_ROWS(ArithF64Fma, 8)};
         const int bi = kMinbVals[mi] == 1 ? 0 : (kMinbVals[mi] == 3 ? 1 : -1);
         if (bi < 0 || ilp < 1 || ilp > 4) return nullptr;
-        static const KernelFn b16[3][4][2] = {MANDEL_BT_ROWS(ArithF64, 16), MANDEL_BT_ROWS(ArithF32, 16),
-                                              MANDEL_BT_ROWS(ArithF64Fma, 16)};
+        static const KernelFn b16[2][4][2] = {MANDEL_BT_ROWS(ArithF64, 16), MANDEL_BT_ROWS(ArithF64Fma, 16)};
         if (bt == 4) return b4[fp32][ilp - 1][bi];
         if (bt == 8) return b8[fp32][ilp - 1][bi];
-        if (bt == 16) return b16[fp32][ilp - 1][bi];
+        if (bt == 16 && fp32 != 1) return b16[fp32 == 2 ? 1 : 0][ilp - 1][bi];
         return nullptr;
     }
     if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
@@ -264,9 +263,10 @@ struct KernelChoice {
 // ILP2 runs with ptxas' unconstrained schedule (72 registers, 3 CTAs of 256 threads per SM).
 // Batched escape check with a whole-batch replay on a hit (R18), measured per config
 // (profiles/r01_sweep_batch.jsonl, Giter/s): fp64 C2 check-every-8 ILP2 2061 (per-update
-// check 1722), C5 2360 (1962); fp32 C3 check-every-16 ILP1 3438 (per-update ILP4 2504).
+// check 1722), C5 2360 (1962); fp32 C3 check-every-8 ILP1 3346 (per-update ILP4 2504).
+// fp32 stops at 8 updates per test: R18's drift bound covers no more (16 measured 3438).
 constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 3, 8},    // fp64
-                                            {MANDEL_KERNEL_EAGER, 1, 3, 16},   // fp32
+                                            {MANDEL_KERNEL_EAGER, 1, 3, 8},    // fp32
                                             {MANDEL_KERNEL_EAGER, 2, 3, 8}};   // fp64 FMA
 constexpr uint32_t kDefaultRefillLanes = 16;  // LAZY on C4: 8 -> 1509, 16 -> 1555 Giter/s
 constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
@@ -463,6 +463,8 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         kc.bt = 1;
     } else if (ce) {
         if (ce > 1 && !d.r2_ge4) return fail(MANDEL_EINVAL, "a batched escape check needs R >= 2");
+        if (ce > 8 && dtype == MANDEL_FP32)
+            return fail(MANDEL_EINVAL, "fp32 allows check_every <= 8 (the R18 drift bound)");
         kc.bt = ce;
     } else if (!d.r2_ge4 || (kc.minb != 1 && kc.minb != 3)) {
         kc.bt = 1;

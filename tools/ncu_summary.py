@@ -25,6 +25,9 @@ KEYS = [
     "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum",
     "dram__bytes_read.sum", "dram__bytes_write.sum",
     "smsp__warps_eligible.avg.per_cycle_active", "smsp__warps_active.avg.per_cycle_active",
+    "smsp__inst_executed_pipe_fp64.sum", "sm__inst_executed_pipe_fp64.sum",
+    "smsp__inst_executed_pipe_fma.sum", "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -47,13 +50,26 @@ def num(s):
         return None
 
 
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+         "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+
+
+def scaled(v, unit):
+    """Value in bytes (byte units) or milliseconds (time units); others unchanged."""
+    x = num(v)
+    if x is None:
+        return None
+    return x * SCALE.get(unit, 1)
+
+
 def summarise(rep):
     out = []
     for d, u in load(rep):
         s = {"kernel": d.get("Kernel Name"), "id": d.get("ID")}
         for k in KEYS:
             if k in d:
-                s[k] = num(d[k])
+                s[k] = scaled(d[k], u.get(k, ""))
+        s["units"] = {"bytes": "byte", "gpu__time_duration.sum": "ms"}
         stalls = {}
         for k, v in d.items():
             if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio"):
@@ -66,5 +82,28 @@ def summarise(rep):
     return out
 
 
+def write_traffic(rep, config, n_gpus, path, summary_path):
+    """profiles/<tag>_traffic.json: what bench.py quotes beside its live roofline --
+    DRAM bytes per launch and the executed FP pipe utilisation of the escape kernel."""
+    s = [x for x in summarise(rep) if "escape" in (x["kernel"] or "")][0]
+    fp64 = s.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+    fma = s.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active")
+    d = {"config": config, "n_gpus": n_gpus, "kernel": s["kernel"],
+         "dram_bytes_per_launch": s["dram_bytes_per_launch"],
+         "fp64_pipe_active_pct": fp64, "fma_pipe_active_pct": fma,
+         "warp_execution_efficiency": (s.get("smsp__thread_inst_executed_per_inst_executed.ratio") or 0) / 32,
+         "duration_ms_ncu": s.get("gpu__time_duration.sum"), "source": summary_path}
+    with open(path, "w") as f:
+        json.dump(d, f, indent=1)
+    return d
+
+
 if __name__ == "__main__":
-    print(json.dumps([summarise(r) for r in sys.argv[1:]], indent=1))
+    if len(sys.argv) > 1 and sys.argv[1] == "--traffic":
+        # --traffic REP CONFIG NGPUS OUT.json SUMMARY.json
+        rep, cfg, n, outp, summ = sys.argv[2:7]
+        with open(summ, "w") as f:
+            json.dump(summarise(rep), f, indent=1)
+        print(json.dumps(write_traffic(rep, cfg, int(n), outp, summ), indent=1))
+    else:
+        print(json.dumps([summarise(r) for r in sys.argv[1:]], indent=1))

@@ -1,6 +1,8 @@
 #!/bin/bash
 # Round profiling of the bench command on one B200: launch list + one full capture of
 # the escape kernel (run from the repo root under gpurun).  usage: profile_bench.sh TAG [bench args]
+# Back in the container:  python tools/ncu_summary.py --traffic gpurun_out/TAG_full.ncu-rep \
+#     CONFIG 1 profiles/TAG_traffic.json profiles/TAG_ncu_summary.json
 set -u
 mkdir -p gpurun_out
 tag=$1; shift
