@@ -35,47 +35,62 @@ class RankRenderer:
     """Rank ``rank`` of ``world`` rendering one configuration into rank 0's map.
 
     ``args`` are the scalar arguments (xmin, xmax, ymin, ymax, W, H, iterMax, R);
-    ``stream`` is the cudaStream_t (int) of this rank's device.
+    ``stream`` is the cudaStream_t (int) of this rank's device.  ``lib`` is the
+    binding module (tests pass a recording stand-in to check the step protocol).
+
+    Step protocol (one barrier per render): the FCFS counter alternates between
+    two slots by step parity.  During step s rank 0 zeroes the slot step s+1 will
+    use (stream-ordered and synchronised before its render returns); the barrier
+    that ends step s then orders that zero before every rank's first claim of
+    step s+1, and no rank still claims from that slot (it was step s-1's, which
+    every rank finished before the previous barrier).
     """
 
     CTR_BYTES = 256
 
-    def __init__(self, dist, rank: int, world: int, device: int, args, dtype: str, stream):
+    def __init__(self, dist, rank: int, world: int, device: int, args, dtype: str, stream, lib=None):
+        self.M = lib if lib is not None else M
         self.dist, self.rank, self.world, self.device = dist, rank, world, device
         self.args, self.dtype, self.stream = tuple(args), dtype, stream
         W, H = int(args[4]), int(args[5])
         self.nbytes = W * H * 4
         self.owned = []
         self.mapped = []
+        self.nstep = 0
+        L = self.M
         if rank == 0:
-            self.img = M.mandel_dev_alloc(device, self.nbytes)
-            self.ctr = M.mandel_dev_alloc(device, self.CTR_BYTES)
-            self.owned = [self.img, self.ctr]
-            handles = (M.mandel_ipc_handle(self.img), M.mandel_ipc_handle(self.ctr))
+            self.img = L.mandel_dev_alloc(device, self.nbytes)
+            ctr = L.mandel_dev_alloc(device, 2 * self.CTR_BYTES)
+            L.mandel_dev_zero(ctr, 2 * self.CTR_BYTES, stream)
+            self.owned = [self.img, ctr]
+            handles = (L.mandel_ipc_handle(self.img), L.mandel_ipc_handle(ctr))
             share_bytes(dist, rank, handles)
         else:
             handles = share_bytes(dist, rank, None)
-            self.img = M.mandel_ipc_open(device, handles[0])
-            self.ctr = M.mandel_ipc_open(device, handles[1])
-            self.mapped = [self.img, self.ctr]
+            self.img = L.mandel_ipc_open(device, handles[0])
+            ctr = L.mandel_ipc_open(device, handles[1])
+            self.mapped = [self.img, ctr]
+        self.ctrs = (ctr, ctr + self.CTR_BYTES)
         dist.barrier()
 
     def step(self, scheme: str, **kw) -> dict:
-        """One render: reset the shared counter (FCFS), line up, render, line up."""
-        if M.SCHEMES[scheme] in (M.MANDEL_FCFS, M.MANDEL_FCFS_MASTER) and self.rank == 0:
-            M.mandel_dev_zero(self.ctr, self.CTR_BYTES, self.stream)
+        """One render: rank 0 readies the next step's counter, every rank renders, line up."""
+        L = self.M
+        cur, nxt = self.ctrs[self.nstep % 2], self.ctrs[(self.nstep + 1) % 2]
+        if self.rank == 0:
+            L.mandel_dev_zero(nxt, self.CTR_BYTES, self.stream)
+        st = L.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world, self.img,
+                                  cur, self.stream, **kw)
         self.dist.barrier()
-        st = M.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world, self.img,
-                                  self.ctr, self.stream, **kw)
-        self.dist.barrier()
+        self.nstep += 1
         return st
 
     def close(self):
         self.dist.barrier()
         for p in self.mapped:
-            M.mandel_ipc_close(p)
+            self.M.mandel_ipc_close(p)
         self.mapped = []
         self.dist.barrier()
         for p in self.owned:
-            M.mandel_dev_free(p)
+            self.M.mandel_dev_free(p)
         self.owned = []

@@ -41,9 +41,84 @@ def _worker(rank, world, port, q):
             dist.all_gather_object(allrows, rows)
             flat = sorted(r for part in allrows for r in part)
             out[f"{scheme}{H}"] = flat == list(range(H))
+        out["protocol"] = _step_protocol(dist, rank, world)
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
+
+
+class _RecordingLib:
+    """Stands in for the binding in RankRenderer: records the calls in order."""
+    MANDEL_FCFS = 2
+
+    def __init__(self, log):
+        self.log, self.next = log, 0x10000
+
+    def mandel_dev_alloc(self, device, nbytes):
+        self.next += 0x100000
+        self.log.append(("alloc", self.next, nbytes))
+        return self.next
+
+    def mandel_dev_zero(self, ptr, nbytes, stream):
+        self.log.append(("zero", ptr, nbytes))
+
+    def mandel_ipc_handle(self, ptr):
+        return ptr.to_bytes(64, "little")
+
+    def mandel_ipc_open(self, device, h):
+        return int.from_bytes(h, "little")
+
+    def mandel_ipc_close(self, ptr):
+        self.log.append(("close", ptr))
+
+    def mandel_dev_free(self, ptr):
+        self.log.append(("free", ptr))
+
+    def mandel_render_rank(self, *a, **kw):
+        self.log.append(("render", a[13], a[12]))  # (counter pointer, image pointer)
+        return {}
+
+
+def _step_protocol(dist, rank, world):
+    """RankRenderer's step protocol: counters alternate by step parity, rank 0 zeroes the
+    next step's counter inside the current step, one barrier per step."""
+    from paper_2007_00745_b200.multiproc import RankRenderer
+    log = []
+    calls = {"barrier": 0}
+    real_barrier = dist.barrier
+
+    class D:
+        def __getattr__(self, k):
+            return getattr(dist, k)
+
+        def barrier(self):
+            calls["barrier"] += 1
+            log.append(("barrier",))
+            real_barrier()
+
+    rr = RankRenderer(D(), rank, world, 0, (-2.5, 1.5, -2.0, 2.0, 64, 48, 100, 2.0), "fp64", 0,
+                      lib=_RecordingLib(log))
+    c0, c1 = rr.ctrs
+    b0 = calls["barrier"]
+    n0 = len(log)
+    for _ in range(4):
+        rr.step("fcfs")
+    steps = log[n0:]
+    ok = calls["barrier"] - b0 == 4 and c1 == c0 + rr.CTR_BYTES
+    renders = [e for e in steps if e[0] == "render"]
+    ok = ok and [e[1] for e in renders] == [c0, c1, c0, c1] and all(e[2] == rr.img for e in renders)
+    if rank == 0:
+        ok = ok and any(e[0] == "zero" and e[1] == c0 and e[2] == 2 * rr.CTR_BYTES for e in log[:n0])
+        # per step: zero(next) -> render(cur) -> barrier
+        want = []
+        for s in range(4):
+            want += [("zero", (c0, c1)[(s + 1) % 2], rr.CTR_BYTES), ("render", (c0, c1)[s % 2], rr.img),
+                     ("barrier",)]
+        ok = ok and steps == want
+    else:
+        ok = ok and not any(e[0] == "zero" for e in log)
+    rr.close()
+    return ok
 
 
 def test_two_rank_plumbing():
@@ -62,3 +137,4 @@ def test_two_rank_plumbing():
         assert res[r]["agg"] == (11.0, 3000)
         for k in ("block8000", "cyclic8000", "block1001", "cyclic1001"):
             assert res[r][k], k
+        assert res[r]["protocol"]
