@@ -67,6 +67,9 @@ def parse():
                     help="target CPU work (core-seconds) of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-schemes", action="store_true", help="skip the per-scheme lines")
+    ap.add_argument("--share-device", action="store_true",
+                    help="TEST ONLY: every rank on cuda:0 with gloo plumbing (checks the N>1 "
+                         "code path on a one-GPU box; not a measurement)")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: warmup + steps only, no e2e/cpu/schemes legs")
     return ap.parse_args()
@@ -167,12 +170,18 @@ def run_ours(args):
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
     dist = None
+    if args.share_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist_mod
-        dist_mod.init_process_group("nccl", device_id=dev)
+        if args.share_device:
+            dist_mod.init_process_group("gloo")
+        else:
+            dist_mod.init_process_group("nccl", device_id=dev)
         dist = dist_mod
+    adev = None if args.share_device else dev  # gloo reduces host tensors
     mandel.lib()
     if args.kernel not in mandel.KERNELS:
         raise SystemExit(f"unknown --kernel {args.kernel}; choose from {sorted(mandel.KERNELS)}")
@@ -231,18 +240,22 @@ def run_ours(args):
     time.sleep(0.3)
     ms, stats = timed(args.scheme, args.steps, args.warmup, sampler)
     sampler.stop()
-    iters_rank = stats[-1]["sum_iters"]
-    assert all(s["sum_iters"] == iters_rank for s in stats), "non-deterministic work per step"
-    tot_ms, iters_job = aggregate(dist, ms, iters_rank, dev)
+    from paper_2007_00745_b200.multiproc import sum_over_ranks
+    iters_rank = stats[-1]["sum_iters"]  # this rank's share of the last step (FCFS: varies)
+    iters_launch = statistics.mean(s["sum_iters"] for s in stats)  # per launch of this rank
+    per_step = sum_over_ranks(dist, [s["sum_iters"] for s in stats], adev)
+    assert all(v == per_step[0] for v in per_step), "the map's work differs between steps"
+    tot_ms, _ = aggregate(dist, ms, 0, adev)
+    iters_job = per_step[0]
     ms_per_step = tot_ms / args.steps
     value = iters_job / (ms_per_step * 1e-3) / 1e9  # Giter/s
     kern_ms = statistics.mean(s["kernel_ms_max"] for s in stats)
-    kern_ms_all, _ = aggregate(dist, kern_ms, 0, dev)
+    kern_ms_all, _ = aggregate(dist, kern_ms, 0, adev)
     clocks = sampler.summary()
 
     # roofline of the dominant kernel (the escape kernel): algorithmic FP ops per launch
     # (8 per pixel-iteration of this rank) / its CUDA-event duration on the launching stream
-    achieved = iters_rank * FLOPS_PER_ITER / (kern_ms * 1e-3) / 1e12
+    achieved = iters_launch * FLOPS_PER_ITER / (kern_ms * 1e-3) / 1e12
     peak = fp_peak_tflops(cfg.dtype)
     roof = {"bound": "alu", "unit": "TFLOP/s", "achieved": round(achieved, 4),
             "peak": round(peak, 4), "frac": round(achieved / peak, 4),
@@ -251,7 +264,7 @@ def run_ours(args):
                           f"{cfg.dtype.upper()} lanes x {SM_MAX_MHZ:.0f} MHz (guide unit counts, "
                           "max clock; DESIGN.md Roofline)",
             "kernel_ms": round(kern_ms, 4),
-            "ops_per_launch": iters_rank * FLOPS_PER_ITER}
+            "ops_per_launch": int(iters_launch * FLOPS_PER_ITER)}
     prof = _traffic_from_profiles(cfg, world)
     if prof:
         # from the committed ncu --set full capture of this kernel (profiles/): DRAM bytes
@@ -300,7 +313,7 @@ def run_ours(args):
             if rank == 0 else None
         ne = max(1, args.e2e_steps)
         ems, _ = timed(args.scheme, ne, 1, None, out_host=host if rank == 0 else None)
-        ems_job, _ = aggregate(dist, ems, 0, dev)
+        ems_job, _ = aggregate(dist, ems, 0, adev)
         e2e_val = iters_job / (ems_job / ne * 1e-3) / 1e9
         line["e2e"] = {"value": round(e2e_val, 3), "unit": "Giter/s", "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": nbytes, "steps": ne,
@@ -317,13 +330,15 @@ def run_ours(args):
                     continue
                 k = max(5, args.steps // 4)
                 sms, sst = timed(sch, k, 2)
-                sms_job, _ = aggregate(dist, sms, 0, dev)
+                sms_job, _ = aggregate(dist, sms, 0, adev)
                 per[sch] = {"value": round(iters_job / (sms_job / k * 1e-3) / 1e9, 3),
                             "ms_per_step": round(sms_job / k, 4), "steps": k}
             line["per_scheme"] = per
 
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds, img)
+    if args.share_device:
+        line["test_only_shared_device"] = True  # N ranks on one GPU: not a measurement
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -31,6 +31,16 @@ def aggregate(dist, rank_ms: float, rank_iters: int, device=None):
     return float(t.item()), int(n.item())
 
 
+def sum_over_ranks(dist, values, device=None):
+    """Element-wise sum over ranks of a list of integers (e.g. per-step iteration counts)."""
+    if dist is None:
+        return [int(v) for v in values]
+    import torch
+    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [int(v) for v in t.tolist()]
+
+
 class RankRenderer:
     """Rank ``rank`` of ``world`` rendering one configuration into rank 0's map.
 
