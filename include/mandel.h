@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 2
+#define MANDEL_ABI_VERSION 3
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -123,14 +123,14 @@ typedef struct mandel_stats {
                                       eager iterations per loop exit (< 10 selects LAZY)           */
     uint64_t warp_iters;           /* kernel-choice probe only (else 0): loop iterations over warps */
     uint64_t loop_exits;           /* kernel-choice probe only (else 0): loop exits over warps      */
-    int32_t  kernel_batch;         /* EAGER: z-updates per escape check actually run (1, 4 or 8)    */
-    int32_t  pad_;
+    int32_t  kernel_batch;         /* EAGER: z-updates per escape check actually run (1, 4, 8, 16)  */
+    int32_t  kernel_packed;        /* 1: the fp32 batched loop ran on FADD2/FMUL2 slot pairs        */
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
 typedef struct mandel_options {
     uint32_t chunk_rows;     /* FCFS rows per claim; 0 -> 16 (BASELINE.json C5)                   */
-    uint32_t tile_px;        /* pixels per warp tile (refill kernel); 0 -> library default        */
+    uint32_t tile_px;        /* pixels per warp tile (persistent kernels); 0 -> 256               */
     int      kernel;         /* enum mandel_kernel                                                */
     int      logical_ranks;  /* nonzero: allow ngpus > device count, rank g runs on device
                                 g % count on its own stream (tests; ranks never wait on each other) */
@@ -142,6 +142,12 @@ typedef struct mandel_options {
     int      adapt_hi;       /* ADAPTIVE: lazy runs before probing eager again; 0 -> default         */
     int      bands;          /* one GPU + out_host: row bands whose device->host copies overlap
                                 the later bands' compute (0 -> 8, 1 -> no pipelining, max 32)     */
+    int      tile_rows;      /* persistent kernels: row slots per warp tile (power of two <= 64;
+                                a tile is tile_rows x tile_px/tile_rows pixels, handed to the
+                                warp in 8-column blocks); FCFS cuts it to divide chunk_rows;
+                                0 -> 8                                                           */
+    int      no_pack;        /* fp32: nonzero keeps the batched loop scalar (default: packed
+                                FADD2/FMUL2 on slot pairs when ilp >= 2; bit-identical)           */
     int      check_every;    /* EAGER: z-updates per escape test.  1 -> every update (Eq. 2 as
                                 written); 4, 8 or 16 -> batched (R18): |z|^2 is tested
                                 after every 4th/8th/16th update against a threshold just below

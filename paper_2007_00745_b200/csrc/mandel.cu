@@ -227,7 +227,8 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
                                                MANDEL_ILP2_ROWS(escape_adaptive_kernel, ArithF64Fma)};
     static const KernelFn statics[3] = {escape_static_kernel<ArithF64>, escape_static_kernel<ArithF32>,
                                         escape_static_kernel<ArithF64Fma>};
-    if (fp32 < 0 || fp32 > 2) return nullptr;
+    if (fp32 < 0 || fp32 > 3) return nullptr;
+    if (fp32 == 3 && !(variant == MANDEL_KERNEL_EAGER && bt > 1)) fp32 = 1;  // packing: batched loop only
     if (variant == MANDEL_KERNEL_STATIC) return statics[fp32];
     if (variant == kVariantProbe) {  // the per-update-check eager kernels with loop statistics
         static const KernelFn probe[3] = {escape_refill_kernel<ArithF64, 2, 1, 1, true>,
@@ -237,16 +238,17 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
     }
     if (mi < 0 || mi > 5) return nullptr;
     if (variant == MANDEL_KERNEL_EAGER && bt > 1) {
-        static const KernelFn b4[3][4][2] = {MANDEL_BT_ROWS(ArithF64, 4), MANDEL_BT_ROWS(ArithF32, 4),
-                                             MANDEL_BT_ROWS(ArithF64Fma, 4)};
-        static const KernelFn b8[3][4][2] = {MANDEL_BT_ROWS(ArithF64, 8), MANDEL_BT_ROWS(ArithF32, 8),
-                                             MANDEL_BT_ROWS(ArithF64Fma, 8)};
+        // row 3: fp32 on packed slot pairs (ArithF32P, NEXT-4b)
+        static const KernelFn b4[4][4][2] = {MANDEL_BT_ROWS(ArithF64, 4), MANDEL_BT_ROWS(ArithF32, 4),
+                                             MANDEL_BT_ROWS(ArithF64Fma, 4), MANDEL_BT_ROWS(ArithF32P, 4)};
+        static const KernelFn b8[4][4][2] = {MANDEL_BT_ROWS(ArithF64, 8), MANDEL_BT_ROWS(ArithF32, 8),
+                                             MANDEL_BT_ROWS(ArithF64Fma, 8), MANDEL_BT_ROWS(ArithF32P, 8)};
         const int bi = kMinbVals[mi] == 1 ? 0 : (kMinbVals[mi] == 3 ? 1 : -1);
         if (bi < 0 || ilp < 1 || ilp > 4) return nullptr;
         static const KernelFn b16[2][4][2] = {MANDEL_BT_ROWS(ArithF64, 16), MANDEL_BT_ROWS(ArithF64Fma, 16)};
         if (bt == 4) return b4[fp32][ilp - 1][bi];
         if (bt == 8) return b8[fp32][ilp - 1][bi];
-        if (bt == 16 && fp32 != 1) return b16[fp32 == 2 ? 1 : 0][ilp - 1][bi];
+        if (bt == 16 && (fp32 == 0 || fp32 == 2)) return b16[fp32 == 2 ? 1 : 0][ilp - 1][bi];
         return nullptr;
     }
     if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
@@ -258,7 +260,8 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
 // MANDEL_KERNEL_REFILL resolves to these configurations (the measured fastest).
 struct KernelChoice {
     int variant, ilp, minb;
-    int bt;  // EAGER: z-updates per escape check (1 = every update; 4, 8 = batched, R18)
+    int bt;          // EAGER: z-updates per escape check (1 = every update; 4, 8, 16 = batched, R18)
+    int packed = 0;  // fp32 batched loop on FADD2/FMUL2 slot pairs (set by build_params)
 };
 // ILP2 runs with ptxas' unconstrained schedule (72 registers, 3 CTAs of 256 threads per SM).
 // Batched escape check with a whole-batch replay on a hit (R18), measured per config
@@ -338,7 +341,8 @@ int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
     return MANDEL_OK;
 }
 
-constexpr uint32_t kDefaultTile = 256;
+constexpr uint32_t kDefaultTile = 256;     // pixels per tile
+constexpr uint32_t kDefaultTileRows = 8;   // rows per tile: 8 x 32 px, streamed as 8 x 8 blocks
 constexpr uint32_t kDefaultChunk = 16;
 
 struct LaunchSpec {
@@ -405,7 +409,16 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     if (kernel == MANDEL_KERNEL_STATIC && is_dynamic(scheme))
         return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
     const uint32_t chunk = effective_chunk(scheme, o);
-    uint32_t tile = (o && o->tile_px) ? o->tile_px : kDefaultTile;
+    // 2-D tiles: tile_rows row slots x (tile_px / tile_rows) columns; an
+    // FCFS tile must stay inside one chunk, so its rows are cut to a power of two
+    // dividing chunk_rows
+    uint32_t trows = (o && o->tile_rows) ? (uint32_t)o->tile_rows : kDefaultTileRows;
+    if (trows > 64 || (trows & (trows - 1)) != 0)
+        return fail(MANDEL_EINVAL, "options.tile_rows must be a power of two <= 64");
+    if (kscheme == MANDEL_FCFS)
+        while (chunk % trows) trows >>= 1;
+    const uint32_t tpx = (o && o->tile_px) ? o->tile_px : kDefaultTile;
+    uint32_t tile = tpx / trows > 0 ? tpx / trows : 1u;
     if (tile > W) tile = W;
     mandel::Params& p = ls.p;
     std::memset(&p, 0, sizeof(p));
@@ -423,11 +436,14 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.scheme = (uint32_t)kscheme;
     p.tile_w = tile;
     p.tiles_per_row = (W + tile - 1) / tile;
+    p.tile_rows = trows;
+    p.tile_shift = 3;
+    while ((1u << p.tile_shift) < trows * 8) ++p.tile_shift;
     p.nslots = pl.nslots; p.base0 = pl.base0; p.stride0 = pl.stride0; p.count0 = pl.count0; p.base1 = pl.base1;
     p.chunk_rows = chunk;
     p.nchunks = (uint32_t)(((uint64_t)H + chunk - 1) / chunk);
     if (kscheme == MANDEL_FCFS) {
-        uint64_t tiles = (uint64_t)(p.nchunks + 1) * chunk * p.tiles_per_row;
+        uint64_t tiles = (uint64_t)(p.nchunks + 1) * (chunk / trows) * p.tiles_per_row;
         if (tiles >= 0xF0000000ull) return fail(MANDEL_EINVAL, "FCFS tile space exceeds 32 bits; raise tile_px");
     } else if ((uint64_t)p.nslots * p.tiles_per_row >= 0xF0000000ull) {
         return fail(MANDEL_EINVAL, "tile space exceeds 32 bits; raise tile_px");
@@ -470,8 +486,13 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         kc.bt = 1;
     }
     const int mi = minb_index(kc.minb);
+    // fp32 batched loops run on packed slot pairs (FADD2/FMUL2) unless options.no_pack
+    const bool packed = dtype == MANDEL_FP32 && kc.variant == MANDEL_KERNEL_EAGER && kc.bt > 1 &&
+                        kc.ilp >= 2 && !(o && o->no_pack);
+    kc.packed = packed ? 1 : 0;
     ls.kc = kc;
-    ls.fn = kernel_fn(fi, kc.variant, kc.ilp, mi, kc.bt);
+    ls.fn = kernel_fn(packed ? 3 : fi, kc.variant, kc.ilp, mi, kc.bt);
+    p.opaque_zero = 0u;
     if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
     const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;  // (the probe variant is persistent)
     int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;
@@ -685,6 +706,7 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         stats->kernel_variant = specs[0].kc.variant;
         stats->kernel_ilp = specs[0].kc.ilp;
         stats->kernel_batch = specs[0].kc.bt;
+        stats->kernel_packed = specs[0].kc.packed;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -842,6 +864,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         stats->kernel_variant = specs[0].kc.variant;
         stats->kernel_ilp = specs[0].kc.ilp;
         stats->kernel_batch = specs[0].kc.bt;
+        stats->kernel_packed = specs[0].kc.packed;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -996,6 +1019,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->kernel_variant = ls.kc.variant;
         stats->kernel_ilp = ls.kc.ilp;
         stats->kernel_batch = ls.kc.bt;
+        stats->kernel_packed = ls.kc.packed;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t0;

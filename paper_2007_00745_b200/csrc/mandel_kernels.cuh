@@ -49,7 +49,10 @@ struct Params {
     uint32_t r2batch;                // batched-check threshold on ukey, below key(R2) (R18)
     uint32_t W, H, iter_max;
     uint32_t scheme;
-    uint32_t tile_w, tiles_per_row;
+    uint32_t tile_w, tiles_per_row;  // columns per tile; tiles per group of tile_rows row slots
+    uint32_t tile_rows;              // row slots per tile (FCFS: divides chunk_rows)
+    uint32_t tile_shift;             // log2(tile_rows * 8)
+    uint32_t opaque_zero;            // 0: ArithF32P's contraction barrier (XOR operand)
     // static schemes: slot s -> row s < count0 ? base0 + s*stride0 : base1 + (s - count0)
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
@@ -69,6 +72,7 @@ struct Params {
 struct ArithF64 {
     typedef double T;
     typedef long long bits_t;
+    static constexpr bool kPacked = false;
     static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
     static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
     static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
@@ -126,6 +130,7 @@ struct ArithF64Fma : ArithF64 {
 struct ArithF32 {
     typedef float T;
     typedef int bits_t;
+    static constexpr bool kPacked = false;
     static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
     static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
     static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
@@ -149,6 +154,61 @@ struct ArithF32 {
     static __device__ __forceinline__ void resq(float x, float y, float& x2, float& y2) {
         x2 = mul(x, x);
         y2 = mul(y, y);
+    }
+};
+
+// MANDEL_FP32 with the batched loop on packed pairs of slots (NEXT-4b): FADD2/FMUL2
+// (PTX add/sub/mul.rn.f32x2, sm_100a) do two slots' RN operations per instruction,
+// bit-identical to the scalar ones.  ptxas contracts a packed multiply feeding a
+// packed add into FFMA2 even with .rn and -fmad=false, so every product passes
+// through an opaque integer XOR with a runtime zero (one LOP3 on its high half)
+// that ptxas cannot see through; the SASS gate test checks no FFMA2 remains.
+struct ArithF32P : ArithF32 {
+    static constexpr bool kPacked = true;
+    typedef unsigned long long u64;
+    static __device__ __forceinline__ u64 pk(float a, float b) {
+        u64 r;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+        return r;
+    }
+    static __device__ __forceinline__ void upk(u64 v, float& a, float& b) {
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    }
+    static __device__ __forceinline__ u64 add2(u64 a, u64 b) {
+        u64 r;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+        return r;
+    }
+    static __device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+        u64 r;
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+        return r;
+    }
+    static __device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+        u64 r;
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+        return r;
+    }
+    // contraction barrier: v with its high half XOR-ed with oz (== 0 at run time)
+    static __device__ __forceinline__ u64 opq(u64 v, uint32_t oz) {
+        uint32_t lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+        hi ^= oz;
+        u64 r;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+        return r;
+    }
+    // Eq. 1 on two slots at once, in the oracle's operation order
+    static __device__ __forceinline__ void step2(float& xa, float& xb, float& ya, float& yb, float& x2a,
+                                                 float& x2b, float& y2a, float& y2b, float cra, float crb,
+                                                 float cia, float cib, uint32_t oz) {
+        const u64 X = pk(xa, xb), Y = pk(ya, yb), X2 = pk(x2a, x2b), Y2 = pk(y2a, y2b);
+        const u64 NY = add2(opq(mul2(add2(X, X), Y), oz), pk(cia, cib));
+        const u64 NX = add2(sub2(X2, Y2), pk(cra, crb));
+        upk(NX, xa, xb);
+        upk(NY, ya, yb);
+        upk(opq(mul2(NX, NX), oz), x2a, x2b);
+        upk(opq(mul2(NY, NY), oz), y2a, y2b);
     }
 };
 
@@ -208,19 +268,58 @@ __device__ __forceinline__ uint32_t wait_bound(const Params& p, uint32_t k) {
     return g;
 }
 
+// A tile: `nrows` row slots x `cols` columns starting at column j0.  `base` is the
+// first slot of the group (static schemes; rows come from the plan) or the first
+// image row (FCFS; the group's rows are consecutive inside one chunk).  Its pixels
+// are streamed in 8-column sub-blocks, row-major inside each (tile_pixel), so the
+// pixels a warp holds at once are a compact 2-D patch: neighbours escape at nearly
+// the same update, which makes escapes -- and the batched test's hits -- coincide.
+struct Tile {
+    uint32_t base, nrows, j0, cols;
+};
+
+__device__ __forceinline__ Tile bcast_tile(const Tile& t) {
+    const unsigned FULL = 0xffffffffu;
+    return Tile{__shfl_sync(FULL, t.base, 0), __shfl_sync(FULL, t.nrows, 0), __shfl_sync(FULL, t.j0, 0),
+                __shfl_sync(FULL, t.cols, 0)};
+}
+
+// Pixel q of tile t -> image (row, col).
+__device__ __forceinline__ void tile_pixel(const Params& p, const Tile& t, uint32_t q, uint32_t& row,
+                                           uint32_t& col) {
+    // full groups (the common case) have a power-of-two height: shift instead of divide
+    const uint32_t band = t.nrows << 3;
+    const uint32_t sub = t.nrows == p.tile_rows ? q >> p.tile_shift : q / band;
+    const uint32_t w = q - sub * band;
+    const uint32_t bw = min(8u, t.cols - (sub << 3));
+    uint32_t dy, dx;
+    if (bw == 8u) {
+        dy = w >> 3;
+        dx = w & 7u;
+    } else {
+        dy = w / bw;
+        dx = w - dy * bw;
+    }
+    col = t.j0 + (sub << 3) + dx;
+    const uint32_t sl = t.base + dy;
+    row = p.scheme == kSchemeFcfs ? sl
+                                  : (sl < p.count0 ? p.base0 + sl * p.stride0 : p.base1 + (sl - p.count0));
+}
+
 // (ck, cg) caches lane 0's last local->global chunk binding, so only the first
 // draw in each chunk reads chunk_map (an L2 round trip) -- init ck = 0xffffffff.
-__device__ __forceinline__ int draw_tile(const Params& p, uint32_t& row, uint32_t& j0, uint32_t& j1,
-                                         uint32_t& ck, uint32_t& cg) {
+__device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck, uint32_t& cg) {
     const uint32_t t = atomicAdd(&p.ws->tile_ctr, 1u);
-    const uint32_t slot = t / p.tiles_per_row;
-    const uint32_t seg = t - slot * p.tiles_per_row;
-    j0 = seg * p.tile_w;
-    j1 = min(j0 + p.tile_w, p.W);
+    const uint32_t grp = t / p.tiles_per_row;
+    const uint32_t seg = t - grp * p.tiles_per_row;
+    const uint32_t slot = grp * p.tile_rows;
+    tl.j0 = seg * p.tile_w;
+    tl.cols = min(p.tile_w, p.W - tl.j0);
     if (p.scheme != kSchemeFcfs) {
         if (slot >= p.nslots) return kTileNone;
-        row = slot < p.count0 ? p.base0 + slot * p.stride0 : p.base1 + (slot - p.count0);
-        if (seg == 0) atomicAdd(&p.ws->rows_started, 1u);
+        tl.base = slot;
+        tl.nrows = min(p.tile_rows, p.nslots - slot);
+        if (seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
         return kTileOk;
     }
     const uint32_t k = slot / p.chunk_rows;
@@ -245,9 +344,11 @@ __device__ __forceinline__ int draw_tile(const Params& p, uint32_t& row, uint32_
     ck = k;
     cg = g;
     if (g == kChunkDone) return kTileNone;
-    row = (g - 1) * p.chunk_rows + r;
+    const uint32_t row = (g - 1) * p.chunk_rows + r;
     if (row >= p.H) return kTileSkip;
-    if (seg == 0) atomicAdd(&p.ws->rows_started, 1u);
+    tl.base = row;
+    tl.nrows = min(p.tile_rows, p.H - row);
+    if (seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
     return kTileOk;
 }
 
@@ -275,11 +376,20 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
 // slot whose final |z|^2 key reaches r2b (below key(R2); R18).
 template <typename A, int ILP, int BT, typename T>
 __device__ __forceinline__ bool batch_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
-                                          const T (&cr)[ILP], const T (&ci)[ILP], uint32_t r2b) {
+                                          const T (&cr)[ILP], const T (&ci)[ILP], uint32_t r2b,
+                                          uint32_t oz) {
 #pragma unroll
     for (int u = 0; u < BT; ++u) {
+        if constexpr (A::kPacked) {
 #pragma unroll
-        for (int s = 0; s < ILP; ++s) A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+            for (int s = 0; s + 1 < ILP; s += 2)
+                A::step2(x[s], x[s + 1], y[s], y[s + 1], x2[s], x2[s + 1], y2[s], y2[s + 1], cr[s], cr[s + 1],
+                         ci[s], ci[s + 1], oz);
+            if (ILP & 1) A::step(x[ILP - 1], y[ILP - 1], x2[ILP - 1], y2[ILP - 1], cr[ILP - 1], ci[ILP - 1]);
+        } else {
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+        }
     }
     uint32_t m = 0;
 #pragma unroll
@@ -329,10 +439,9 @@ escape_refill_kernel(const Params p) {
     unsigned long long my_iters = 0, my_pix = 0;
     uint32_t w_iters = 0, w_exits = 0;  // warp-uniform loop statistics (wrap-free below 2^32)
 
-    // warp-uniform tile cursor: columns [jcur, jend) of row trow
-    uint32_t jcur = 0, jend = 0;
-    T ci_tile = zero;            // Cy[trow] = ymax - trow*dy
-    uint32_t* row_ptr = p.out;   // &out[trow * W]
+    // warp-uniform tile cursor: pixels [tq, tqend) of tile tl
+    Tile tl = {0u, 0u, 0u, 0u};
+    uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
     unsigned need[ILP];
@@ -350,34 +459,32 @@ escape_refill_kernel(const Params p) {
         if (nd) {
             uint32_t served = 0;
             for (;;) {
-                if (jcur >= jend) {
+                if (tq >= tqend) {
                     if (!more) break;
                     int st = 0;
-                    uint32_t r_ = 0, a_ = 0, b_ = 0;
-                    if (lane == 0) st = draw_tile(p, r_, a_, b_, ck_, cg_);
+                    if (lane == 0) st = draw_tile(p, tl, ck_, cg_);
                     st = __shfl_sync(FULL, st, 0);
                     if (st == kTileNone) { more = false; break; }
                     if (st == kTileSkip) continue;
-                    const uint32_t trow = __shfl_sync(FULL, r_, 0);
-                    jcur = __shfl_sync(FULL, a_, 0);
-                    jend = __shfl_sync(FULL, b_, 0);
-                    ci_tile = A::sub(ymax, A::mul(A::cvt(trow), dy));  // Cy[i] = ymax - i*dy
-                    row_ptr = p.out + (size_t)trow * p.W;
+                    tl = bcast_tile(tl);
+                    tq = 0;
+                    tqend = tl.nrows * tl.cols;
                 }
-                const uint32_t take = min(jend - jcur, nd - served);
+                const uint32_t take = min(tqend - tq, nd - served);
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
                     const uint32_t q = rank[s] - served;
                     if (((need[s] >> lane) & 1u) && q < take) {
-                        const uint32_t j = jcur + q;
+                        uint32_t i, j;
+                        tile_pixel(p, tl, tq + q, i, j);
                         cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
-                        ci[s] = ci_tile;
+                        ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
                         x[s] = y[s] = x2[s] = y2[s] = zero;
                         rem[s] = p.iter_max;
-                        dst[s] = row_ptr + j;
+                        dst[s] = p.out + ((size_t)i * p.W + j);
                     }
                 }
-                jcur += take;
+                tq += take;
                 served += take;
                 if (served == nd) break;
             }
@@ -427,7 +534,7 @@ escape_refill_kernel(const Params p) {
                             sx[s] = x[s];
                             sy[s] = y[s];
                         }
-                        hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b);
+                        hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero);
                         if (hit) break;
                         k += BT;
                         if (kmax - k < BT) break;
@@ -612,7 +719,8 @@ escape_lazy_kernel(const Params p) {
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
-    uint32_t trow = 0, jcur = 0, jend = 0;  // warp-uniform tile cursor
+    Tile tl = {0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
+    uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
     unsigned need[ILP];
@@ -629,34 +737,33 @@ escape_lazy_kernel(const Params p) {
         }
         uint32_t served = 0;
         while (served < nd) {
-            if (jcur >= jend) {
+            if (tq >= tqend) {
                 if (!more) break;
                 int st = 0;
-                uint32_t r_ = 0, a_ = 0, b_ = 0;
-                if (lane == 0) st = draw_tile(p, r_, a_, b_, ck_, cg_);
+                if (lane == 0) st = draw_tile(p, tl, ck_, cg_);
                 st = __shfl_sync(FULL, st, 0);
                 if (st == kTileNone) { more = false; break; }
                 if (st == kTileSkip) continue;
-                trow = __shfl_sync(FULL, r_, 0);
-                jcur = __shfl_sync(FULL, a_, 0);
-                jend = __shfl_sync(FULL, b_, 0);
+                tl = bcast_tile(tl);
+                tq = 0;
+                tqend = tl.nrows * tl.cols;
             }
-            const uint32_t take = min(jend - jcur, nd - served);
-            const T ci_row = A::sub(ymax, A::mul(A::cvt(trow), dy));  // Cy[i] = ymax - i*dy
+            const uint32_t take = min(tqend - tq, nd - served);
 #pragma unroll
             for (int s = 0; s < ILP; ++s) {
                 if (((need[s] >> lane) & 1u) && rank[s] >= served && rank[s] < served + take) {
-                    const uint32_t j = jcur + (rank[s] - served);
+                    uint32_t i, j;
+                    tile_pixel(p, tl, tq + (rank[s] - served), i, j);
                     cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
-                    ci[s] = ci_row;
+                    ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
                     x[s] = y[s] = x2[s] = y2[s] = zero;
                     n[s] = 0;
                     lv[s] = 1;
                     has[s] = true;
-                    dst[s] = p.out + ((size_t)trow * p.W + j);
+                    dst[s] = p.out + ((size_t)i * p.W + j);
                 }
             }
-            jcur += take;
+            tq += take;
             served += take;
         }
         // ---- iterate until enough slots are finished (or a deadline)
@@ -735,9 +842,8 @@ escape_adaptive_kernel(const Params p) {
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
-    uint32_t jcur = 0, jend = 0;
-    T ci_tile = zero;
-    uint32_t* row_ptr = p.out;
+    Tile tl = {0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
+    uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
     bool lazy = false;           // warp-uniform run mode
@@ -758,34 +864,32 @@ escape_adaptive_kernel(const Params p) {
         if (nd) {
             uint32_t served = 0;
             for (;;) {
-                if (jcur >= jend) {
+                if (tq >= tqend) {
                     if (!more) break;
                     int st = 0;
-                    uint32_t r_ = 0, a_ = 0, b_ = 0;
-                    if (lane == 0) st = draw_tile(p, r_, a_, b_, ck_, cg_);
+                    if (lane == 0) st = draw_tile(p, tl, ck_, cg_);
                     st = __shfl_sync(FULL, st, 0);
                     if (st == kTileNone) { more = false; break; }
                     if (st == kTileSkip) continue;
-                    const uint32_t trow = __shfl_sync(FULL, r_, 0);
-                    jcur = __shfl_sync(FULL, a_, 0);
-                    jend = __shfl_sync(FULL, b_, 0);
-                    ci_tile = A::sub(ymax, A::mul(A::cvt(trow), dy));  // Cy[i] = ymax - i*dy
-                    row_ptr = p.out + (size_t)trow * p.W;
+                    tl = bcast_tile(tl);
+                    tq = 0;
+                    tqend = tl.nrows * tl.cols;
                 }
-                const uint32_t take = min(jend - jcur, nd - served);
+                const uint32_t take = min(tqend - tq, nd - served);
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
                     const uint32_t q = rank[s] - served;
                     if (((need[s] >> lane) & 1u) && q < take) {
-                        const uint32_t j = jcur + q;
+                        uint32_t i, j;
+                        tile_pixel(p, tl, tq + q, i, j);
                         cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
-                        ci[s] = ci_tile;
+                        ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
                         x[s] = y[s] = x2[s] = y2[s] = zero;
                         rem[s] = p.iter_max;
-                        dst[s] = row_ptr + j;
+                        dst[s] = p.out + ((size_t)i * p.W + j);
                     }
                 }
-                jcur += take;
+                tq += take;
                 served += take;
                 if (served == nd) break;
             }

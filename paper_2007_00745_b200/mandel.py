@@ -73,7 +73,7 @@ class mandel_stats(ctypes.Structure):
         ("warp_iters", ctypes.c_uint64),
         ("loop_exits", ctypes.c_uint64),
         ("kernel_batch", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("kernel_packed", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -92,7 +92,7 @@ class mandel_stats(ctypes.Structure):
                 int(self.kernel_variant), str(self.kernel_variant)),
             "kernel_ilp": int(self.kernel_ilp), "probe": [float(v) for v in self.probe],
             "warp_iters": int(self.warp_iters), "loop_exits": int(self.loop_exits),
-            "kernel_batch": int(self.kernel_batch),
+            "kernel_batch": int(self.kernel_batch), "kernel_packed": int(self.kernel_packed),
         }
 
 
@@ -108,6 +108,8 @@ class mandel_options(ctypes.Structure):
         ("adapt_lo", ctypes.c_int),
         ("adapt_hi", ctypes.c_int),
         ("bands", ctypes.c_int),
+        ("tile_rows", ctypes.c_int),
+        ("no_pack", ctypes.c_int),
         ("check_every", ctypes.c_int),
     ]
 
@@ -202,7 +204,8 @@ def _ptr(a) -> int | None:
 
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
-          refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0):
+          refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
+          tile_rows=0, no_pack=False):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -216,6 +219,8 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.adapt_hi = adapt_hi or 0
     o.bands = bands or 0
     o.check_every = check_every or 0
+    o.tile_rows = tile_rows or 0
+    o.no_pack = 1 if no_pack else 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -246,13 +251,13 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      ngpus=1, *, out_host=None, out_dev0=None, stream0=None, chunk_rows=0,
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
-                     bands=0, check_every=0) -> dict:
+                     bands=0, check_every=0, tile_rows=0, no_pack=False) -> dict:
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict."""
     st = mandel_stats()
     o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
-              adapt_hi, bands, check_every)
+              adapt_hi, bands, check_every, tile_rows, no_pack)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st))
@@ -263,12 +268,13 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
 def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, rank, nranks,
                        out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
                        kernel=MANDEL_KERNEL_REFILL, refill_lanes=0, ilp=0,
-                       min_ctas=0, adapt_lo=0, adapt_hi=0, check_every=0) -> dict:
+                       min_ctas=0, adapt_lo=0, adapt_hi=0, check_every=0, tile_rows=0,
+                       no_pack=False) -> dict:
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
     pointers valid in this process (own, or mapped with mandel_ipc_open)."""
     st = mandel_stats()
     o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas, adapt_lo, adapt_hi,
-              0, check_every)
+              0, check_every, tile_rows, no_pack)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
                                   _ptr(out_root), _ptr(fcfs_counter), stream, ctypes.byref(st))

@@ -106,7 +106,8 @@ def test_random_small_configs(mandel, oracle, dtype, kernel):
         ce = 1 if (_batched(mandel, kernel) and cfg.R < 2.0) else 0  # R18 needs R >= 2
         out, st = _render_dev(mandel, cfg, scheme, ngpus, tile_px=[0, 1, 7, 32, 33][k % 5],
                               chunk_rows=[0, 1, 3][k % 3], kernel=kernel,
-                              refill_lanes=[0, 1, 3, 16, 32][k % 5], check_every=ce)
+                              refill_lanes=[0, 1, 3, 16, 32][k % 5], check_every=ce,
+                              tile_rows=[0, 1, 2, 4, 8, 16, 32][k % 7])
         _assert_same(_host(out), want, f"{cfg.name}/{dtype}/{scheme}/N={ngpus}")
         assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
 
@@ -175,6 +176,50 @@ def test_batched_check_adversarial(mandel, oracle, cfg, kernel):
         assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
         if kernel != "refill":
             assert st["kernel_batch"] == mandel.KERNELS[kernel][2]
+
+
+@pytest.mark.parametrize("tile_rows", [1, 2, 4, 8, 16, 64])
+@pytest.mark.parametrize("kernel", ["refill", "refill1", "lazy2", "adaptive2", "batch8x2"])
+@pytest.mark.parametrize("scheme", ["block", "cyclic", "fcfs"])
+def test_tile_rows(mandel, oracle, tile_rows, kernel, scheme):
+    # 2-D tiles: tile_rows row slots streamed in 8-column blocks; ragged in both directions
+    cfg = wl.C1.with_(W=203, H=77, iter_max=600)
+    want = oracle.render(cfg)
+    for ngpus, tile_px, chunk in ((1, 0, 0), (3, 100, 0), (2, 37, 4), (5, 512, 3)):
+        out, st = _render_dev(mandel, cfg, scheme, ngpus, kernel=kernel, tile_rows=tile_rows,
+                              tile_px=tile_px, chunk_rows=chunk)
+        _assert_same(_host(out), want, f"tile_rows={tile_rows}/{kernel}/{scheme}/N={ngpus}")
+        assert st["sum_iters"] == int(want.sum(dtype=np.uint64)) and st["pixels"] == cfg.pixels
+        if scheme != "fcfs":
+            assert st["rank_rows"] == [len(x) for x in (
+                mandel.mandel_plan_rows(scheme, cfg.H, ngpus, r) for r in range(ngpus))]
+        else:
+            assert sum(st["rank_rows"]) == cfg.H
+
+
+def test_tile_rows_invalid(mandel):
+    cfg = wl.C1.with_(W=64, H=64)
+    for bad in (3, 6, 128):
+        with pytest.raises(mandel.MandelError):
+            _render_dev(mandel, cfg, "block", 1, tile_rows=bad)
+
+
+@pytest.mark.parametrize("kernel", ["batch4x2", "batch8x2", "batch8x3", "batch8x4", "batch4x4"])
+def test_fp32_packed_loop(mandel, oracle, kernel):
+    # NEXT-4b: the fp32 batched loop on FADD2/FMUL2 slot pairs is bit-identical to the
+    # scalar loop and the oracle (odd ILP packs all but the last slot)
+    for k, cfg in enumerate(wl.random_small_configs(20, 7, "fp32")):
+        if cfg.R < 2.0:
+            cfg = cfg.with_(R=2.0)
+        want = oracle.render(cfg)
+        for no_pack in (False, True):
+            out, st = _render_dev(mandel, cfg, ["fcfs", "block", "cyclic"][k % 3], 1 + k % 3,
+                                  kernel=kernel, no_pack=no_pack, tile_rows=[1, 8][k % 2])
+            _assert_same(_host(out), want, f"{cfg.name}/{kernel}/no_pack={no_pack}")
+            assert st["kernel_packed"] == (0 if no_pack else 1)
+    cfg = wl.C1.with_(dtype="fp32", iter_max=3000)
+    out, _ = _render_dev(mandel, cfg, "fcfs", 1, kernel=kernel)
+    _assert_same(_host(out), oracle.render(cfg), f"C1 fp32 packed {kernel}")
 
 
 @pytest.mark.parametrize("R,batch", [(2.0, 8), (1.9999999999999998, 1), (1.5, 1), (20.0, 8)])

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--kernels", default="refill1,refill2")
     ap.add_argument("--schemes", default="block,fcfs")
     ap.add_argument("--tiles", default="256")
+    ap.add_argument("--tile-rows", default="0", help="rows per tile, comma separated (0 = default)")
+    ap.add_argument("--pack", default="1", help="fp32 packed batched loop: 1, 0 or 1,0")
     ap.add_argument("--chunks", default="16")
     ap.add_argument("--lanes", default="8")
     ap.add_argument("--minb", default="1")
@@ -45,9 +47,10 @@ def main():
             cfg = cfg.with_(dtype=a.dtype)
         ref = None
         out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
-        for kern, scheme, tile, chunk, lanes, minb, adapt in itertools.product(
-                a.kernels.split(","), a.schemes.split(","), a.tiles.split(","), a.chunks.split(","),
-                a.lanes.split(","), a.minb.split(","), a.adapt.split(",")):
+        for kern, scheme, tile, trows, chunk, lanes, minb, adapt, pack in itertools.product(
+                a.kernels.split(","), a.schemes.split(","), a.tiles.split(","), a.tile_rows.split(","),
+                a.chunks.split(","), a.lanes.split(","), a.minb.split(","), a.adapt.split(","),
+                a.pack.split(",")):
             if not kern.startswith("adaptive") and adapt != a.adapt.split(",")[0]:
                 continue
             alo, ahi = (int(v) for v in adapt.split(":"))
@@ -58,7 +61,8 @@ def main():
             if kern == "static" and minb != a.minb.split(",")[0]:
                 continue
             kw = dict(out_dev0=out, stream0=stream.cuda_stream, kernel=kern,
-                      tile_px=int(tile), chunk_rows=int(chunk), refill_lanes=int(lanes),
+                      tile_px=int(tile), tile_rows=int(trows), chunk_rows=int(chunk), refill_lanes=int(lanes),
+                      no_pack=pack == "0",
                       min_ctas=int(minb) if kern != "static" else 0, adapt_lo=alo, adapt_hi=ahi)
             out.zero_()
             for _ in range(a.warmup):
@@ -82,7 +86,8 @@ def main():
             # pixel-iterations/s at the FP pipe peak: 8 ops/iteration (6 for the FMA dtype)
             ops = 6 if cfg.dtype == "fp64fma" else 8
             peak = 148 * (128 if cfg.dtype == "fp32" else 64) * 1.965e9 / ops / 1e9
-            print(json.dumps({"config": name, "dtype": cfg.dtype, "kernel": kern, "scheme": scheme, "tile": int(tile),
+            print(json.dumps({"config": name, "dtype": cfg.dtype, "kernel": kern, "scheme": scheme, "tile": int(tile), "tile_rows": int(trows),
+                              "packed": st["kernel_packed"], "batch": st["kernel_batch"],
                               "chunk": int(chunk), "lanes": int(lanes), "minb": int(minb), "adapt": adapt, "ms": round(ms, 4),
                               "kernel_ms": round(sum(ks) / len(ks), 4),
                               "giter_s": round(giter, 2), "frac": round(giter / peak, 4),
