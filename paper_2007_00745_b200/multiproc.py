@@ -48,20 +48,23 @@ class RankRenderer:
     ``stream`` is the cudaStream_t (int) of this rank's device.  ``lib`` is the
     binding module (tests pass a recording stand-in to check the step protocol).
 
-    Step protocol (one barrier per render): the FCFS counter alternates between
-    two slots by step parity.  During step s rank 0 zeroes the slot step s+1 will
-    use (stream-ordered and synchronised before its render returns); the barrier
-    that ends step s then orders that zero before every rank's first claim of
-    step s+1, and no rank still claims from that slot (it was step s-1's, which
-    every rank finished before the previous barrier).
+    Step protocol.  Rank 0 owns ``slots`` FCFS counters (one per render, zeroed
+    together); render n claims from counter n mod slots, so consecutive renders
+    never share a counter and need no barrier between them: a rank that finishes
+    render n early starts render n+1 at once (the map is rewritten with the same
+    values).  When the slots run out, every rank lines up, rank 0 zeroes them all
+    and every rank lines up again.  ``step(barrier=True)`` ends a render with a
+    barrier -- needed when the caller reads the whole map right after it (e2e).
     """
 
     CTR_BYTES = 256
 
-    def __init__(self, dist, rank: int, world: int, device: int, args, dtype: str, stream, lib=None):
+    def __init__(self, dist, rank: int, world: int, device: int, args, dtype: str, stream, lib=None,
+                 slots: int = 512):
         self.M = lib if lib is not None else M
         self.dist, self.rank, self.world, self.device = dist, rank, world, device
         self.args, self.dtype, self.stream = tuple(args), dtype, stream
+        self.slots = slots
         W, H = int(args[4]), int(args[5])
         self.nbytes = W * H * 4
         self.owned = []
@@ -70,8 +73,8 @@ class RankRenderer:
         L = self.M
         if rank == 0:
             self.img = L.mandel_dev_alloc(device, self.nbytes)
-            ctr = L.mandel_dev_alloc(device, 2 * self.CTR_BYTES)
-            L.mandel_dev_zero(ctr, 2 * self.CTR_BYTES, stream)
+            ctr = L.mandel_dev_alloc(device, slots * self.CTR_BYTES)
+            L.mandel_dev_zero(ctr, slots * self.CTR_BYTES, stream)
             self.owned = [self.img, ctr]
             handles = (L.mandel_ipc_handle(self.img), L.mandel_ipc_handle(ctr))
             share_bytes(dist, rank, handles)
@@ -80,19 +83,25 @@ class RankRenderer:
             self.img = L.mandel_ipc_open(device, handles[0])
             ctr = L.mandel_ipc_open(device, handles[1])
             self.mapped = [self.img, ctr]
-        self.ctrs = (ctr, ctr + self.CTR_BYTES)
+        self.ctr = ctr
         dist.barrier()
 
-    def step(self, scheme: str, **kw) -> dict:
-        """One render: rank 0 readies the next step's counter, every rank renders, line up."""
+    def counter(self, n: int) -> int:
+        return self.ctr + (n % self.slots) * self.CTR_BYTES
+
+    def step(self, scheme: str, barrier: bool = False, **kw) -> dict:
+        """One render into rank 0's map (see the class notes for the protocol)."""
         L = self.M
-        cur, nxt = self.ctrs[self.nstep % 2], self.ctrs[(self.nstep + 1) % 2]
-        if self.rank == 0:
-            L.mandel_dev_zero(nxt, self.CTR_BYTES, self.stream)
+        if self.nstep and self.nstep % self.slots == 0:  # every counter used once: recycle
+            self.dist.barrier()
+            if self.rank == 0:
+                L.mandel_dev_zero(self.ctr, self.slots * self.CTR_BYTES, self.stream)
+            self.dist.barrier()
         st = L.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world, self.img,
-                                  cur, self.stream, **kw)
-        self.dist.barrier()
+                                  self.counter(self.nstep), self.stream, **kw)
         self.nstep += 1
+        if barrier:
+            self.dist.barrier()
         return st
 
     def close(self):

@@ -80,11 +80,11 @@ class _RecordingLib:
 
 
 def _step_protocol(dist, rank, world):
-    """RankRenderer's step protocol: counters alternate by step parity, rank 0 zeroes the
-    next step's counter inside the current step, one barrier per step."""
+    """RankRenderer's step protocol: one zeroed counter slot per render, no barrier between
+    renders, all slots recycled (barrier, zero, barrier) when used up; barrier=True ends a
+    render with a barrier."""
     from paper_2007_00745_b200.multiproc import RankRenderer
     log = []
-    calls = {"barrier": 0}
     real_barrier = dist.barrier
 
     class D:
@@ -92,31 +92,27 @@ def _step_protocol(dist, rank, world):
             return getattr(dist, k)
 
         def barrier(self):
-            calls["barrier"] += 1
             log.append(("barrier",))
             real_barrier()
 
     rr = RankRenderer(D(), rank, world, 0, (-2.5, 1.5, -2.0, 2.0, 64, 48, 100, 2.0), "fp64", 0,
-                      lib=_RecordingLib(log))
-    c0, c1 = rr.ctrs
-    b0 = calls["barrier"]
+                      lib=_RecordingLib(log), slots=3)
+    B = rr.CTR_BYTES
+    ok = True
+    if rank == 0:  # all three slots zeroed once at set-up
+        ok = ok and ("zero", rr.ctr, 3 * B) in log
     n0 = len(log)
-    for _ in range(4):
+    for _ in range(7):
         rr.step("fcfs")
+    rr.step("fcfs", barrier=True)
     steps = log[n0:]
-    ok = calls["barrier"] - b0 == 4 and c1 == c0 + rr.CTR_BYTES
-    renders = [e for e in steps if e[0] == "render"]
-    ok = ok and [e[1] for e in renders] == [c0, c1, c0, c1] and all(e[2] == rr.img for e in renders)
-    if rank == 0:
-        ok = ok and any(e[0] == "zero" and e[1] == c0 and e[2] == 2 * rr.CTR_BYTES for e in log[:n0])
-        # per step: zero(next) -> render(cur) -> barrier
-        want = []
-        for s in range(4):
-            want += [("zero", (c0, c1)[(s + 1) % 2], rr.CTR_BYTES), ("render", (c0, c1)[s % 2], rr.img),
-                     ("barrier",)]
-        ok = ok and steps == want
-    else:
-        ok = ok and not any(e[0] == "zero" for e in log)
+    want = []
+    for n in range(8):
+        if n and n % 3 == 0:
+            want += [("barrier",)] + ([("zero", rr.ctr, 3 * B)] if rank == 0 else []) + [("barrier",)]
+        want.append(("render", rr.ctr + (n % 3) * B, rr.img))
+    want.append(("barrier",))
+    ok = ok and steps == want
     rr.close()
     return ok
 

@@ -41,14 +41,14 @@ def _worker(rank, world, port, cfg, schemes, q):
     try:
         torch.cuda.set_device(0)
         stream = torch.cuda.current_stream(0).cuda_stream
-        rr = RankRenderer(dist, rank, world, 0, cfg.args(), cfg.dtype, stream)
+        rr = RankRenderer(dist, rank, world, 0, cfg.args(), cfg.dtype, stream, slots=4)
         res = {}
         for scheme in schemes:
-            for rep in range(3):  # several steps: the FCFS counter slots alternate
+            for rep in range(3):  # several renders: counter slots are used in turn and recycled
                 if rank == 0:  # a zeroed map: every pixel must be (re)written by some rank
                     M.mandel_dev_zero(rr.img, cfg.W * cfg.H * 4, stream)
                 dist.barrier()
-                st = rr.step(scheme)
+                st = rr.step(scheme, barrier=True)
                 _, iters = aggregate(dist, st["kernel_ms_max"], st["sum_iters"])
                 if rank == 0:
                     host = torch.empty((cfg.H, cfg.W), dtype=torch.int32, pin_memory=True)
