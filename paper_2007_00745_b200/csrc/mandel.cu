@@ -253,6 +253,24 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
     }
     if (variant == MANDEL_KERNEL_EAGER && ilp >= 1 && ilp <= 4) return eager[fp32][ilp - 1][mi];
     if (variant == MANDEL_KERNEL_LAZY && ilp >= 1 && ilp <= 2) return lazy[fp32][ilp - 1][mi];
+    if (variant == MANDEL_KERNEL_ADAPTIVE && bt > 1) {  // ADAPTIVE on the batched EAGER runs
+        static const KernelFn ab[3][2][2][2] = {
+            {{{escape_adaptive_kernel<ArithF64, 1, 1, 4>, escape_adaptive_kernel<ArithF64, 1, 3, 4>},
+              {escape_adaptive_kernel<ArithF64, 1, 1, 8>, escape_adaptive_kernel<ArithF64, 1, 3, 8>}},
+             {{escape_adaptive_kernel<ArithF64, 2, 1, 4>, escape_adaptive_kernel<ArithF64, 2, 3, 4>},
+              {escape_adaptive_kernel<ArithF64, 2, 1, 8>, escape_adaptive_kernel<ArithF64, 2, 3, 8>}}},
+            {{{escape_adaptive_kernel<ArithF32, 1, 1, 4>, escape_adaptive_kernel<ArithF32, 1, 3, 4>},
+              {escape_adaptive_kernel<ArithF32, 1, 1, 8>, escape_adaptive_kernel<ArithF32, 1, 3, 8>}},
+             {{escape_adaptive_kernel<ArithF32, 2, 1, 4>, escape_adaptive_kernel<ArithF32, 2, 3, 4>},
+              {escape_adaptive_kernel<ArithF32, 2, 1, 8>, escape_adaptive_kernel<ArithF32, 2, 3, 8>}}},
+            {{{escape_adaptive_kernel<ArithF64Fma, 1, 1, 4>, escape_adaptive_kernel<ArithF64Fma, 1, 3, 4>},
+              {escape_adaptive_kernel<ArithF64Fma, 1, 1, 8>, escape_adaptive_kernel<ArithF64Fma, 1, 3, 8>}},
+             {{escape_adaptive_kernel<ArithF64Fma, 2, 1, 4>, escape_adaptive_kernel<ArithF64Fma, 2, 3, 4>},
+              {escape_adaptive_kernel<ArithF64Fma, 2, 1, 8>, escape_adaptive_kernel<ArithF64Fma, 2, 3, 8>}}}};
+        const int bi = kMinbVals[mi] == 1 ? 0 : (kMinbVals[mi] == 3 ? 1 : -1);
+        if (bi < 0 || ilp < 1 || ilp > 2 || (bt != 4 && bt != 8) || fp32 > 2) return nullptr;
+        return ab[fp32][ilp - 1][bt == 8][bi];
+    }
     if (variant == MANDEL_KERNEL_ADAPTIVE && ilp >= 1 && ilp <= 2) return adaptive[fp32][ilp - 1][mi];
     return nullptr;
 }
@@ -474,8 +492,8 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     const int ce = o ? o->check_every : 0;
     if (ce < 0 || (ce > 1 && ce != 4 && ce != 8 && ce != 16))
         return fail(MANDEL_EINVAL, "options.check_every must be 0, 1, 4, 8 or 16");
-    if (kc.variant != MANDEL_KERNEL_EAGER) {
-        if (ce > 1 && !force) return fail(MANDEL_EINVAL, "check_every > 1 needs the EAGER kernel");
+    if (kc.variant != MANDEL_KERNEL_EAGER && kc.variant != MANDEL_KERNEL_ADAPTIVE) {
+        if (ce > 1 && !force) return fail(MANDEL_EINVAL, "check_every > 1 needs the EAGER or ADAPTIVE kernel");
         kc.bt = 1;
     } else if (ce) {
         if (ce > 1 && !d.r2_ge4) return fail(MANDEL_EINVAL, "a batched escape check needs R >= 2");

@@ -398,6 +398,132 @@ __device__ __forceinline__ bool batch_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP]
 }
 
 // ---------------------------------------------------------------------------
+// One EAGER run of a warp: iterate Eq. 1 on every slot until some slot finishes
+// (or the smallest remaining budget kmax runs out).  Returns the run length k;
+// fin[s] marks finished slots and kx[s] the iterations slot s performed in the run.
+// ---------------------------------------------------------------------------
+template <typename A, int ILP, int BT, typename T>
+__device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP],
+                                              T (&y2)[ILP], const T (&cr)[ILP], const T (&ci)[ILP],
+                                              const uint32_t (&rem)[ILP], bool (&fin)[ILP],
+                                              uint32_t (&kx)[ILP], uint32_t kmax) {
+    typedef typename A::bits_t B;
+    const unsigned FULL = 0xffffffffu;
+    const B r2 = (B)p.r2bits;
+    const int r2c = p.r2cand;
+    const uint32_t r2b = p.r2batch;
+    bool esc[ILP];
+    // ---- iterate: Eq. 1 on every slot until some slot is finished.  The hot loop
+    // tests a 32-bit candidate key (one compare per slot); on a candidate the warp
+    // leaves the loop and verifies the exact 64-bit test, resuming on a false alarm.
+    // BT > 1 (batched check, R18): BT z-updates per test and |z|^2 only
+    // after the last one, against a threshold below R2 that every slot which escaped
+    // inside the batch still exceeds (|z| grows after an escape when R >= 2); on a
+    // hit the warp restores the batch-start state and replays the batch with the
+    // exact per-update test, so each recorded count is the slot's first escaping
+    // update.  Budget tails shorter than BT run the per-update loop below.
+    uint32_t k = 0;
+    bool lazy_exit = false;
+    for (;;) {
+        if (BT > 1) {
+            // only z = (x, y) is saved at the batch start; on a hit A::resq rebuilds
+            // the carried squares from it with the same operations (identical bits),
+            // and the whole batch is replayed with the exact per-update test, each
+            // slot's escaping update recorded in-loop; every slot that escaped in the
+            // batch is then retired at once
+            while (kmax - k >= BT) {
+                T sx[ILP], sy[ILP];
+                bool hit;
+                for (;;) {  // the hot loop: BT updates, one test
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) {
+                        sx[s] = x[s];
+                        sy[s] = y[s];
+                    }
+                    hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero);
+                    if (hit) break;
+                    k += BT;
+                    if (kmax - k < BT) break;
+                }
+                if (!hit) break;
+                uint32_t ne[ILP], lv[ILP];
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) {
+                    x[s] = sx[s];
+                    y[s] = sy[s];
+                    A::resq(x[s], y[s], x2[s], y2[s]);
+                    lv[s] = rem[s] != kIdleRem ? 1u : 0u;
+                    ne[s] = 0;
+                }
+#pragma unroll
+                for (int u = 0; u < BT; ++u) {
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) {
+                        A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+                        const bool in_ = !(A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2);
+                        ne[s] += lv[s];
+                        lv[s] = in_ ? lv[s] : 0u;
+                    }
+                }
+                bool any_esc = false;
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) {
+                    fin[s] = rem[s] != kIdleRem && lv[s] == 0u;
+                    kx[s] = k + ne[s];
+                    any_esc |= fin[s];
+                }
+                k += BT;
+                if (__any_sync(FULL, any_esc)) {
+                    lazy_exit = true;
+                    break;
+                }
+                // a false alarm (no slot escaped): keep batching from the batch end
+            }
+            if (lazy_exit) break;
+        }
+        const uint32_t lim = kmax;
+        // per-update test up to the end of the budget (tails shorter than BT, BT = 1)
+        while (k < lim) {
+            if (lim - k >= 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    bool e = false;
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
+#pragma unroll
+                    for (int s = 0; s < ILP; ++s) e |= esc[s];
+                    if (__any_sync(FULL, e)) { k += u + 1; goto left_loop; }
+                }
+                k += 4;
+            } else {
+                bool e = false;
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) e |= esc[s];
+                k += 1;
+                if (__any_sync(FULL, e)) break;
+            }
+        }
+    left_loop:
+        bool any_fin = false;
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            // exact Eq. 2 test on the candidate's own |z|^2 (same operands, same bits);
+            // idle slots hold z = 0 and never pass it
+            fin[s] = A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2;
+            any_fin |= fin[s];
+        }
+        if (k == kmax || __any_sync(FULL, any_fin)) break;
+    }
+#pragma unroll
+    for (int s = 0; s < ILP; ++s)
+        if (!(lazy_exit && fin[s])) kx[s] = k;
+
+    return k;
+}
+
+// ---------------------------------------------------------------------------
 // K1/K2: persistent escape kernel with a per-warp tile queue and lane refill.
 // Each lane holds ILP independent pixels ("slots"); their z-updates are
 // interleaved so the FP64 dependency chains of one warp overlap.  The warp
@@ -414,26 +540,20 @@ __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     typedef AR A;
     typedef typename AR::T T;
-    typedef typename A::bits_t B;
     const unsigned FULL = 0xffffffffu;
     const uint32_t lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const B r2 = (B)p.r2bits;
-    const int r2c = p.r2cand;
-    const uint32_t r2b = p.r2batch;
     const T xmin = A::xmin(p), ymax = A::ymax(p), dx = A::dx(p), dy = A::dy(p);
     const T zero = T(0);
 
     // per-slot state; rem == kIdleRem marks an idle slot (z = c = 0: never a candidate)
     T x[ILP], y[ILP], x2[ILP], y2[ILP], cr[ILP], ci[ILP];
     uint32_t rem[ILP];
-    bool esc[ILP];
     uint32_t* dst[ILP];
 #pragma unroll
     for (int s = 0; s < ILP; ++s) {
         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
         rem[s] = kIdleRem;
-        esc[s] = false;
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
@@ -505,114 +625,9 @@ escape_refill_kernel(const Params p) {
         const uint32_t kmax = __reduce_min_sync(FULL, mrem);
         if (kmax == kIdleRem) break;  // every slot of the warp is idle: done
 
-        // ---- iterate: Eq. 1 on every slot until some slot is finished.  The hot loop
-        // tests a 32-bit candidate key (one compare per slot); on a candidate the warp
-        // leaves the loop and verifies the exact 64-bit test, resuming on a false alarm.
-        // BT > 1 (batched check, R18): BT z-updates per test and |z|^2 only
-        // after the last one, against a threshold below R2 that every slot which escaped
-        // inside the batch still exceeds (|z| grows after an escape when R >= 2); on a
-        // hit the warp restores the batch-start state and replays the batch with the
-        // exact per-update test, so each recorded count is the slot's first escaping
-        // update.  Budget tails shorter than BT run the per-update loop below.
-        uint32_t k = 0;
         bool fin[ILP];
-        uint32_t kx[ILP];     // per-slot iterations of this run (differs from k for lazy-replay escapes)
-        bool lazy_exit = false;
-        for (;;) {
-            if (BT > 1) {
-                // only z = (x, y) is saved at the batch start; on a hit A::resq rebuilds
-                // the carried squares from it with the same operations (identical bits),
-                // and the whole batch is replayed with the exact per-update test, each
-                // slot's escaping update recorded in-loop; every slot that escaped in the
-                // batch is then retired at once
-                while (kmax - k >= BT) {
-                    T sx[ILP], sy[ILP];
-                    bool hit;
-                    for (;;) {  // the hot loop: BT updates, one test
-#pragma unroll
-                        for (int s = 0; s < ILP; ++s) {
-                            sx[s] = x[s];
-                            sy[s] = y[s];
-                        }
-                        hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero);
-                        if (hit) break;
-                        k += BT;
-                        if (kmax - k < BT) break;
-                    }
-                    if (!hit) break;
-                    uint32_t ne[ILP], lv[ILP];
-#pragma unroll
-                    for (int s = 0; s < ILP; ++s) {
-                        x[s] = sx[s];
-                        y[s] = sy[s];
-                        A::resq(x[s], y[s], x2[s], y2[s]);
-                        lv[s] = rem[s] != kIdleRem ? 1u : 0u;
-                        ne[s] = 0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < BT; ++u) {
-#pragma unroll
-                        for (int s = 0; s < ILP; ++s) {
-                            A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
-                            const bool in_ = !(A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2);
-                            ne[s] += lv[s];
-                            lv[s] = in_ ? lv[s] : 0u;
-                        }
-                    }
-                    bool any_esc = false;
-#pragma unroll
-                    for (int s = 0; s < ILP; ++s) {
-                        fin[s] = rem[s] != kIdleRem && lv[s] == 0u;
-                        kx[s] = k + ne[s];
-                        any_esc |= fin[s];
-                    }
-                    k += BT;
-                    if (__any_sync(FULL, any_esc)) {
-                        lazy_exit = true;
-                        break;
-                    }
-                    // a false alarm (no slot escaped): keep batching from the batch end
-                }
-                if (lazy_exit) break;
-            }
-            const uint32_t lim = kmax;
-            // per-update test up to the end of the budget (tails shorter than BT, BT = 1)
-            while (k < lim) {
-                if (lim - k >= 4) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        bool e = false;
-#pragma unroll
-                        for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
-#pragma unroll
-                        for (int s = 0; s < ILP; ++s) e |= esc[s];
-                        if (__any_sync(FULL, e)) { k += u + 1; goto left_loop; }
-                    }
-                    k += 4;
-                } else {
-                    bool e = false;
-#pragma unroll
-                    for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
-#pragma unroll
-                    for (int s = 0; s < ILP; ++s) e |= esc[s];
-                    k += 1;
-                    if (__any_sync(FULL, e)) break;
-                }
-            }
-        left_loop:
-            bool any_fin = false;
-#pragma unroll
-            for (int s = 0; s < ILP; ++s) {
-                // exact Eq. 2 test on the candidate's own |z|^2 (same operands, same bits);
-                // idle slots hold z = 0 and never pass it
-                fin[s] = A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2;
-                any_fin |= fin[s];
-            }
-            if (k == kmax || __any_sync(FULL, any_fin)) break;
-        }
-#pragma unroll
-        for (int s = 0; s < ILP; ++s)
-            if (!(lazy_exit && fin[s])) kx[s] = k;
+        uint32_t kx[ILP];  // per-slot iterations of this run (differs from k for batch-replay escapes)
+        const uint32_t k = eager_run<A, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax);
 
         if (LSTATS) {
             w_iters += k;
@@ -815,7 +830,7 @@ escape_lazy_kernel(const Params p) {
         lv[s] = in_ ? lv[s] : 0u;                                          \
     } while (0)
 
-template <typename AR, int ILP, int MINB>
+template <typename AR, int ILP, int MINB, int BT = 1>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_adaptive_kernel(const Params p) {
     typedef AR A;
@@ -825,20 +840,17 @@ escape_adaptive_kernel(const Params p) {
     const uint32_t lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const B r2 = (B)p.r2bits;
-    const int r2c = p.r2cand;
     const T xmin = A::xmin(p), ymax = A::ymax(p), dx = A::dx(p), dy = A::dy(p);
     const T zero = T(0);
     const int max_live_full = 32 - (int)p.refill_lanes;
 
     T x[ILP], y[ILP], x2[ILP], y2[ILP], cr[ILP], ci[ILP];
     uint32_t rem[ILP];
-    bool esc[ILP];
     uint32_t* dst[ILP];
 #pragma unroll
     for (int s = 0; s < ILP; ++s) {
         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
         rem[s] = kIdleRem;
-        esc[s] = false;
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
@@ -912,43 +924,12 @@ escape_adaptive_kernel(const Params p) {
         uint32_t k = 0;
         bool fin[ILP];
         if (!lazy) {
-            // ---- eager run (candidate key, exact verification; see escape_refill_kernel)
-            for (;;) {
-                for (;;) {
-                    if (kmax - k >= 4) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            bool e = false;
-#pragma unroll
-                            for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
-#pragma unroll
-                            for (int s = 0; s < ILP; ++s) e |= esc[s];
-                            if (__any_sync(FULL, e)) { k += u + 1; goto eager_left; }
-                        }
-                        k += 4;
-                        if (k == kmax) break;
-                    } else {
-                        bool e = false;
-#pragma unroll
-                        for (int s = 0; s < ILP; ++s) MANDEL_STEP_SLOT(s);
-#pragma unroll
-                        for (int s = 0; s < ILP; ++s) e |= esc[s];
-                        k += 1;
-                        if (__any_sync(FULL, e) || k == kmax) break;
-                    }
-                }
-            eager_left:
-                bool any_fin = false;
-#pragma unroll
-                for (int s = 0; s < ILP; ++s) {
-                    fin[s] = A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2;
-                    any_fin |= fin[s];
-                }
-                if (k == kmax || __any_sync(FULL, any_fin)) break;
-            }
+            // ---- eager run (per-update or batched test; see eager_run)
+            uint32_t kx[ILP];
+            k = eager_run<A, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax);
 #pragma unroll
             for (int s = 0; s < ILP; ++s)
-                if (rem[s] != kIdleRem) rem[s] -= k;
+                if (rem[s] != kIdleRem) rem[s] -= kx[s];
             ema = ema - (ema >> 2) + k;  // ema/4 tracks the eager run length
             if ((ema >> 2) < p.adapt_lo) {
                 lazy = true;

@@ -35,7 +35,9 @@ KERNELS = {"refill": (0, 0), "static": (1, 0), "eager": (2, 0), "lazy": (3, 0),
            # EAGER with the batched escape check (check_every 4 / 8; R18)
            "batch4x1": (2, 1, 4), "batch4x2": (2, 2, 4), "batch4x4": (2, 4, 4),
            "batch8x1": (2, 1, 8), "batch8x2": (2, 2, 8), "batch8x3": (2, 3, 8), "batch8x4": (2, 4, 8),
-           "batch16x1": (2, 1, 16), "batch16x2": (2, 2, 16), "batch16x4": (2, 4, 16)}
+           "batch16x1": (2, 1, 16), "batch16x2": (2, 2, 16), "batch16x4": (2, 4, 16),
+           # ADAPTIVE on batched EAGER runs (lazy runs where escapes are dense)
+           "adaptb4x1": (4, 1, 4), "adaptb4x2": (4, 2, 4), "adaptb8x1": (4, 1, 8), "adaptb8x2": (4, 2, 8)}
 MANDEL_MAX_GPUS = 64
 MANDEL_IPC_HANDLE_BYTES = 64
 

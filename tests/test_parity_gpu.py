@@ -52,7 +52,7 @@ def _assert_same(got, want, label):
 # ---------------------------------------------------------------------------
 KERNELS = ["refill", "refill1", "refill2", "refill3", "refill4", "lazy1", "lazy2", "adaptive1", "adaptive2",
            "batch4x1", "batch4x2", "batch4x4", "batch8x1", "batch8x2", "batch8x3", "batch8x4",
-           "batch16x1", "batch16x2", "batch16x4"]
+           "batch16x1", "batch16x2", "batch16x4", "adaptb4x1", "adaptb8x2"]
 
 
 def _batched(mandel, kernel):
@@ -164,7 +164,7 @@ BATCH_CASES = [
 
 
 @pytest.mark.parametrize("kernel", ["refill", "batch4x1", "batch4x2", "batch8x2", "batch8x4",
-                                    "batch16x1", "batch16x2"])
+                                    "batch16x1", "batch16x2", "adaptb8x2", "adaptb4x1"])
 @pytest.mark.parametrize("cfg", BATCH_CASES, ids=[c.name for c in BATCH_CASES])
 def test_batched_check_adversarial(mandel, oracle, cfg, kernel):
     if cfg.dtype == "fp32" and kernel.startswith("batch16"):
@@ -179,7 +179,7 @@ def test_batched_check_adversarial(mandel, oracle, cfg, kernel):
 
 
 @pytest.mark.parametrize("tile_rows", [1, 2, 4, 8, 16, 64])
-@pytest.mark.parametrize("kernel", ["refill", "refill1", "lazy2", "adaptive2", "batch8x2"])
+@pytest.mark.parametrize("kernel", ["refill", "refill1", "lazy2", "adaptive2", "batch8x2", "adaptb8x2"])
 @pytest.mark.parametrize("scheme", ["block", "cyclic", "fcfs"])
 def test_tile_rows(mandel, oracle, tile_rows, kernel, scheme):
     # 2-D tiles: tile_rows row slots streamed in 8-column blocks; ragged in both directions

@@ -51,12 +51,12 @@ def main():
                 a.kernels.split(","), a.schemes.split(","), a.tiles.split(","), a.tile_rows.split(","),
                 a.chunks.split(","), a.lanes.split(","), a.minb.split(","), a.adapt.split(","),
                 a.pack.split(",")):
-            if not kern.startswith("adaptive") and adapt != a.adapt.split(",")[0]:
+            if not kern.startswith("adapt") and adapt != a.adapt.split(",")[0]:
                 continue
             alo, ahi = (int(v) for v in adapt.split(":"))
             if kern == "static" and scheme == "fcfs":
                 continue
-            if not kern.startswith(("lazy", "adaptive")) and lanes != a.lanes.split(",")[0]:
+            if not kern.startswith(("lazy", "adapt")) and lanes != a.lanes.split(",")[0]:
                 continue
             if kern == "static" and minb != a.minb.split(",")[0]:
                 continue
