@@ -20,6 +20,10 @@
 
 namespace mandel {
 
+#ifndef MANDEL_LAZY_UNROLL
+#define MANDEL_LAZY_UNROLL 16
+#endif
+
 constexpr uint32_t kWarpsPerCta = 8;
 constexpr uint32_t kCtaThreads = kWarpsPerCta * 32;
 constexpr uint32_t kChunkDone = 0xffffffffu;  // chunk_map entry: counter exhausted
@@ -677,7 +681,11 @@ escape_refill_kernel(const Params p) {
         lv[s] = in_ ? lv[s] : 0u;                                          \
     } while (0)
 
-template <typename AR, int ILP, bool DRAIN, typename T = typename AR::T>
+// LU: updates between two exit tests (the lanes-free ballot); the exit is a
+// refill decision only, so testing every LU updates changes no count.  C4 (LAZY,
+// refill_lanes 16): LU 2 -> 1543, 4 -> 1664, 8 -> 1696, 16 -> 1728 Giter/s
+// (profiles/r01g_sweep_lazy_unroll.jsonl).
+template <typename AR, int ILP, bool DRAIN, int LU = MANDEL_LAZY_UNROLL, typename T = typename AR::T>
 __device__ __forceinline__ void lazy_run(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
                                          const T (&cr)[ILP], const T (&ci)[ILP],
                                          uint32_t (&n)[ILP], uint32_t (&lv)[ILP],
@@ -687,12 +695,13 @@ __device__ __forceinline__ void lazy_run(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP],
     const unsigned FULL = 0xffffffffu;
     uint32_t k = 0;
     for (;;) {
-        if (kmax - k >= 2) {
+        if (kmax - k >= LU) {
 #pragma unroll
-            for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
+            for (int u = 0; u < LU; ++u) {
 #pragma unroll
-            for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
-            k += 2;
+                for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
+            }
+            k += LU;
         } else {
 #pragma unroll
             for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
