@@ -67,6 +67,9 @@ def parse():
                     help="target CPU work (core-seconds) of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-schemes", action="store_true", help="skip the per-scheme lines")
+    ap.add_argument("--gather", choices=["fused", "nccl"], default="fused",
+                    help="N>1: fused peer stores into rank 0's map (default) or the NCCL path "
+                         "(rank bands, point-to-point to rank 0, K4 row scatter)")
     ap.add_argument("--share-device", action="store_true",
                     help="TEST ONLY: every rank on cuda:0 with gloo plumbing (checks the N>1 "
                          "code path on a one-GPU box; not a measurement)")
@@ -196,8 +199,12 @@ def run_ours(args):
         img = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
         img_ptr = img.data_ptr()
     else:
-        from paper_2007_00745_b200.multiproc import RankRenderer
-        rr = RankRenderer(dist, rank, world, local, cfg.args(), cfg.dtype, s_handle)
+        from paper_2007_00745_b200.multiproc import GatherRenderer, RankRenderer
+        if args.gather == "nccl":
+            rr = GatherRenderer(dist, rank, world, local, cfg.args(), cfg.dtype, s_handle,
+                                chunk_rows=args.chunk_rows)
+        else:
+            rr = RankRenderer(dist, rank, world, local, cfg.args(), cfg.dtype, s_handle)
         img_ptr = rr.img
         img = None
 
@@ -300,6 +307,10 @@ def run_ours(args):
             "scheme": args.scheme, "chunk_rows": args.chunk_rows, "kernel": args.kernel,
             "sum_iters_per_step": iters_job, "pixels": cfg.pixels,
             "parallelism": f"{args.scheme} rows over {world} GPU(s)",
+            "gather": "none (1 GPU)" if world == 1 else (
+                "fused: every rank's kernel stores into rank 0's map over NVLink (CUDA IPC)"
+                if args.gather == "fused" else
+                "nccl: rank bands sent point-to-point to rank 0, K4 row scatter"),
             "l2": f"no input reads; each step writes a {nbytes / 2**20:.0f} MiB map "
                   "(> 126 MB L2) -- nothing to flush",
         },

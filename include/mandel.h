@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 3
+#define MANDEL_ABI_VERSION 4
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -146,6 +146,14 @@ typedef struct mandel_options {
                                 a tile is tile_rows x tile_px/tile_rows pixels, handed to the
                                 warp in 8-column blocks); FCFS cuts it to divide chunk_rows;
                                 0 -> 8                                                           */
+    int      band_out;       /* mandel_render_rank only (the NCCL gather path):
+                                out_root is this rank's own compact band on its device, band row
+                                b = the rank's b-th row slot (static: the plan's order; FCFS: local
+                                chunk k row r at b = k*chunk_rows + r); mandel_band_rows then gives
+                                each band row's image row, and mandel_scatter_rows (K4) places a
+                                gathered band in the image.  Capacity: static schemes the plan's
+                                row count x W; FCFS ceil(H/chunk_rows)*chunk_rows x W (a rank may
+                                claim every chunk).  mandel_render_ex -> MANDEL_EINVAL            */
     int      no_pack;        /* fp32: nonzero keeps the batched loop scalar (default: packed
                                 FADD2/FMUL2 on slot pairs when ilp >= 2; bit-identical)           */
     int      check_every;    /* EAGER: z-updates per escape test.  1 -> every update (Eq. 2 as
@@ -276,6 +284,24 @@ const char *mandel_last_error(void);
 int mandel_device_count(void);
 /* Frees cached device buffers, streams and events on every device. */
 void mandel_shutdown(void);
+/*
+ * mandel_band_rows -- after a band_out mandel_render_rank call (SURVEY.md §8(e) NCCL path):
+ * the image row of every band row of that render, in band order; 0xffffffff marks a
+ * band row no pixel was written to (FCFS slots past the last image row).  Host memory;
+ * rows_out NULL queries *count.  EINVAL if *count is too small (*count is set).
+ */
+int mandel_band_rows(uint32_t *rows_out, uint32_t *count);
+
+/*
+ * mandel_scatter_rows -- K4: image[rows[b]] = band[b] for b < nrows, W uint32 per row;
+ * rows[b] == 0xffffffff skipped.  band_dev, rows_dev and image_dev are device pointers on
+ * stream's device (stream NULL: image_dev's device, legacy stream).  Asynchronous on
+ * stream.  The de-interleave step after the NCCL gather of cyclic / FCFS bands
+ * ("reconstructs the image").
+ */
+int mandel_scatter_rows(const uint32_t *band_dev, const uint32_t *rows_dev, uint32_t nrows, uint32_t W,
+                        uint32_t *image_dev, void *stream);
+
 /* MANDEL_ABI_VERSION of the loaded library. */
 int mandel_abi_version(void);
 

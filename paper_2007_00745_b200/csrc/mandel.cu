@@ -6,6 +6,7 @@
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
 //        -Xcompiler -fPIC,-ffp-contract=off -shared -Iinclude -o libmandel.so mandel.cu
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <map>
@@ -179,6 +180,7 @@ struct Root {
 };
 
 std::mutex g_mu;
+std::vector<uint32_t> g_band_rows;  // image row of each band row of the last band-mode render
 std::atomic<bool> g_busy{false};
 std::vector<DeviceCtx> g_dev;
 RankCtx g_rank[MANDEL_MAX_GPUS];
@@ -511,6 +513,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     ls.kc = kc;
     ls.fn = kernel_fn(packed ? 3 : fi, kc.variant, kc.ilp, mi, kc.bt);
     p.opaque_zero = 0u;
+    p.band = (o && o->band_out) ? 1u : 0u;
     if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
     const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;  // (the probe variant is persistent)
     int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;
@@ -747,6 +750,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     if (!is_dynamic(scheme) && H < (uint32_t)ngpus) return fail(MANDEL_EINVAL, "static schemes need H >= ngpus");
     if (opts && opts->kernel == MANDEL_KERNEL_STATIC && is_dynamic(scheme))
         return fail(MANDEL_EINVAL, "the static kernel has no work queue: FCFS needs the refill kernel");
+    if (opts && opts->band_out) return fail(MANDEL_EINVAL, "band_out is a mandel_render_rank option");
     int ndev = 0;
     rc = device_count(ndev);
     if (rc) return rc;
@@ -1013,7 +1017,34 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     CK(cudaEventRecord(rk.k1, s));
     mandel::WorkState ws;
     CK(cudaMemcpyAsync(&ws, rk.state, sizeof(ws), cudaMemcpyDeviceToHost, s));
+    const bool band = opts && opts->band_out;
+    std::vector<uint32_t> cmap;
+    if (band && ls.p.scheme == MANDEL_FCFS) {
+        cmap.resize((size_t)ls.p.nchunks + 1);
+        CK(cudaMemcpyAsync(cmap.data(), ls.p.chunk_map, cmap.size() * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaStreamSynchronize(s));
+    if (band) {
+        // the band's row list (K4's input): static schemes -> the plan, slot by slot;
+        // FCFS -> local chunk k holds global chunk cmap[k]-1 (bound in local order)
+        g_band_rows.clear();
+        if (ls.p.scheme == MANDEL_FCFS) {
+            const uint32_t c = ls.p.chunk_rows;
+            for (uint32_t k = 0; k <= ls.p.nchunks; ++k) {
+                const uint32_t g = cmap[k];
+                if (g == 0 || g == mandel::kChunkDone) break;
+                for (uint32_t r = 0; r < c; ++r) {
+                    const uint64_t row = (uint64_t)(g - 1) * c + r;
+                    g_band_rows.push_back(row < H ? (uint32_t)row : 0xffffffffu);
+                }
+            }
+        } else {
+            for (uint32_t sl = 0; sl < ls.p.nslots; ++sl)
+                g_band_rows.push_back(sl < ls.p.count0 ? ls.p.base0 + sl * ls.p.stride0
+                                                      : ls.p.base1 + (sl - ls.p.count0));
+        }
+    }
     if (stats) {
         std::memset(stats, 0, sizeof(*stats));
         float ms = 0;
@@ -1042,6 +1073,43 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t0;
     }
+    return MANDEL_OK;
+}
+
+int mandel_band_rows(uint32_t* rows_out, uint32_t* count) {
+    if (!count) return fail(MANDEL_EINVAL, "count must not be NULL");
+    std::lock_guard<std::mutex> lk(g_mu);
+    const uint32_t n = (uint32_t)g_band_rows.size();
+    if (rows_out) {
+        if (*count < n) {
+            *count = n;
+            return fail(MANDEL_EINVAL, "rows_out capacity too small");
+        }
+        std::memcpy(rows_out, g_band_rows.data(), (size_t)n * sizeof(uint32_t));
+    }
+    *count = n;
+    return MANDEL_OK;
+}
+
+int mandel_scatter_rows(const uint32_t* band_dev, const uint32_t* rows_dev, uint32_t nrows, uint32_t W,
+                        uint32_t* image_dev, void* stream) {
+    if (nrows == 0) return MANDEL_OK;
+    if (!band_dev || !rows_dev || !image_dev || W == 0)
+        return fail(MANDEL_EINVAL, "scatter_rows needs device pointers and W >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    if (s) CK(cudaStreamGetDevice(s, &dev));
+    else {
+        cudaPointerAttributes a;
+        CK(cudaPointerGetAttributes(&a, image_dev));
+        dev = a.device;
+    }
+    CK(cudaSetDevice(dev));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned grid = (unsigned)std::min<uint64_t>(nrows, (uint64_t)sms * 8);
+    mandel::scatter_rows_kernel<<<grid, 256, 0, s>>>(band_dev, rows_dev, nrows, W, image_dev);
+    CK(cudaGetLastError());
     return MANDEL_OK;
 }
 

@@ -17,6 +17,26 @@ namespace mandel {
 
 enum : int { kColorGray = 0, kColorClassic = 1 };
 
+// K4 (the NCCL gather path): copy band row b of a gathered rank band
+// to image row rows[b] (rows[b] == 0xffffffff: an unused slot, skipped).  One CTA per
+// band row group, 16-B vector copies when the row is 16-B aligned.  HBM-bound.
+__global__ void scatter_rows_kernel(const uint32_t* __restrict__ band, const uint32_t* __restrict__ rows,
+                                    uint32_t nrows, uint32_t W, uint32_t* __restrict__ image) {
+    for (uint32_t b = blockIdx.x; b < nrows; b += gridDim.x) {
+        const uint32_t r = rows[b];
+        if (r == 0xffffffffu) continue;
+        const uint32_t* src = band + (size_t)b * W;
+        uint32_t* dst = image + (size_t)r * W;
+        if ((W & 3u) == 0u && (((uintptr_t)src | (uintptr_t)dst) & 15u) == 0u) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            for (uint32_t j = threadIdx.x; j < W / 4; j += blockDim.x) d4[j] = s4[j];
+        } else {
+            for (uint32_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = src[j];
+        }
+    }
+}
+
 __device__ __forceinline__ uint32_t colour_rgb(uint32_t n, uint32_t iter_max, int mode) {
     if (n >= iter_max) return 0u;
     uint32_t r, g, b;

@@ -57,6 +57,7 @@ struct Params {
     uint32_t tile_rows;              // row slots per tile (FCFS: divides chunk_rows)
     uint32_t tile_shift;             // log2(tile_rows * 8)
     uint32_t opaque_zero;            // 0: ArithF32P's contraction barrier (XOR operand)
+    uint32_t band;                   // 1: out is this rank's compact band (row = local slot)
     // static schemes: slot s -> row s < count0 ? base0 + s*stride0 : base1 + (s - count0)
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
@@ -280,17 +281,19 @@ __device__ __forceinline__ uint32_t wait_bound(const Params& p, uint32_t k) {
 // the same update, which makes escapes -- and the batched test's hits -- coincide.
 struct Tile {
     uint32_t base, nrows, j0, cols;
+    uint32_t slot;  // the rank's local slot of the first row (its band row in band mode)
 };
 
 __device__ __forceinline__ Tile bcast_tile(const Tile& t) {
     const unsigned FULL = 0xffffffffu;
     return Tile{__shfl_sync(FULL, t.base, 0), __shfl_sync(FULL, t.nrows, 0), __shfl_sync(FULL, t.j0, 0),
-                __shfl_sync(FULL, t.cols, 0)};
+                __shfl_sync(FULL, t.cols, 0), __shfl_sync(FULL, t.slot, 0)};
 }
 
-// Pixel q of tile t -> image (row, col).
+// Pixel q of tile t -> image (row, col) and the row of the output buffer it is stored
+// to: the image row, or (band mode) the rank-local band row = its local slot.
 __device__ __forceinline__ void tile_pixel(const Params& p, const Tile& t, uint32_t q, uint32_t& row,
-                                           uint32_t& col) {
+                                           uint32_t& col, uint32_t& orow) {
     // full groups (the common case) have a power-of-two height: shift instead of divide
     const uint32_t band = t.nrows << 3;
     const uint32_t sub = t.nrows == p.tile_rows ? q >> p.tile_shift : q / band;
@@ -308,6 +311,7 @@ __device__ __forceinline__ void tile_pixel(const Params& p, const Tile& t, uint3
     const uint32_t sl = t.base + dy;
     row = p.scheme == kSchemeFcfs ? sl
                                   : (sl < p.count0 ? p.base0 + sl * p.stride0 : p.base1 + (sl - p.count0));
+    orow = p.band ? t.slot + dy : row;
 }
 
 // (ck, cg) caches lane 0's last local->global chunk binding, so only the first
@@ -322,6 +326,7 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
     if (p.scheme != kSchemeFcfs) {
         if (slot >= p.nslots) return kTileNone;
         tl.base = slot;
+        tl.slot = slot;
         tl.nrows = min(p.tile_rows, p.nslots - slot);
         if (seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
         return kTileOk;
@@ -351,6 +356,7 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
     const uint32_t row = (g - 1) * p.chunk_rows + r;
     if (row >= p.H) return kTileSkip;
     tl.base = row;
+    tl.slot = slot;
     tl.nrows = min(p.tile_rows, p.H - row);
     if (seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
     return kTileOk;
@@ -564,7 +570,7 @@ escape_refill_kernel(const Params p) {
     uint32_t w_iters = 0, w_exits = 0;  // warp-uniform loop statistics (wrap-free below 2^32)
 
     // warp-uniform tile cursor: pixels [tq, tqend) of tile tl
-    Tile tl = {0u, 0u, 0u, 0u};
+    Tile tl = {0u, 0u, 0u, 0u, 0u};
     uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
@@ -599,13 +605,13 @@ escape_refill_kernel(const Params p) {
                 for (int s = 0; s < ILP; ++s) {
                     const uint32_t q = rank[s] - served;
                     if (((need[s] >> lane) & 1u) && q < take) {
-                        uint32_t i, j;
-                        tile_pixel(p, tl, tq + q, i, j);
+                        uint32_t i, j, o;
+                        tile_pixel(p, tl, tq + q, i, j, o);
                         cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
                         ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
                         x[s] = y[s] = x2[s] = y2[s] = zero;
                         rem[s] = p.iter_max;
-                        dst[s] = p.out + ((size_t)i * p.W + j);
+                        dst[s] = p.out + ((size_t)o * p.W + j);
                     }
                 }
                 tq += take;
@@ -743,7 +749,7 @@ escape_lazy_kernel(const Params p) {
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
-    Tile tl = {0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
+    Tile tl = {0u, 0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
     uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
@@ -776,15 +782,15 @@ escape_lazy_kernel(const Params p) {
 #pragma unroll
             for (int s = 0; s < ILP; ++s) {
                 if (((need[s] >> lane) & 1u) && rank[s] >= served && rank[s] < served + take) {
-                    uint32_t i, j;
-                    tile_pixel(p, tl, tq + (rank[s] - served), i, j);
+                    uint32_t i, j, o;
+                    tile_pixel(p, tl, tq + (rank[s] - served), i, j, o);
                     cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
                     ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
                     x[s] = y[s] = x2[s] = y2[s] = zero;
                     n[s] = 0;
                     lv[s] = 1;
                     has[s] = true;
-                    dst[s] = p.out + ((size_t)i * p.W + j);
+                    dst[s] = p.out + ((size_t)o * p.W + j);
                 }
             }
             tq += take;
@@ -863,7 +869,7 @@ escape_adaptive_kernel(const Params p) {
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
-    Tile tl = {0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
+    Tile tl = {0u, 0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
     uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
@@ -901,13 +907,13 @@ escape_adaptive_kernel(const Params p) {
                 for (int s = 0; s < ILP; ++s) {
                     const uint32_t q = rank[s] - served;
                     if (((need[s] >> lane) & 1u) && q < take) {
-                        uint32_t i, j;
-                        tile_pixel(p, tl, tq + q, i, j);
+                        uint32_t i, j, o;
+                        tile_pixel(p, tl, tq + q, i, j, o);
                         cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
                         ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
                         x[s] = y[s] = x2[s] = y2[s] = zero;
                         rem[s] = p.iter_max;
-                        dst[s] = p.out + ((size_t)i * p.W + j);
+                        dst[s] = p.out + ((size_t)o * p.W + j);
                     }
                 }
                 tq += take;

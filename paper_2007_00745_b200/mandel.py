@@ -111,6 +111,7 @@ class mandel_options(ctypes.Structure):
         ("adapt_hi", ctypes.c_int),
         ("bands", ctypes.c_int),
         ("tile_rows", ctypes.c_int),
+        ("band_out", ctypes.c_int),
         ("no_pack", ctypes.c_int),
         ("check_every", ctypes.c_int),
     ]
@@ -166,6 +167,10 @@ def lib():
             L.mandel_dev_zero.restype = i32
             L.mandel_ipc_close.argtypes = [vp]
             L.mandel_ipc_close.restype = i32
+            L.mandel_band_rows.argtypes = [vp, vp]
+            L.mandel_band_rows.restype = i32
+            L.mandel_scatter_rows.argtypes = [vp, vp, u32, u32, vp, vp]
+            L.mandel_scatter_rows.restype = i32
             _lib = L
     return _lib
 
@@ -207,7 +212,7 @@ def _ptr(a) -> int | None:
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
-          tile_rows=0, no_pack=False):
+          tile_rows=0, no_pack=False, band_out=False):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -223,6 +228,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.check_every = check_every or 0
     o.tile_rows = tile_rows or 0
     o.no_pack = 1 if no_pack else 0
+    o.band_out = 1 if band_out else 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -271,12 +277,12 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
                        out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
                        kernel=MANDEL_KERNEL_REFILL, refill_lanes=0, ilp=0,
                        min_ctas=0, adapt_lo=0, adapt_hi=0, check_every=0, tile_rows=0,
-                       no_pack=False) -> dict:
+                       no_pack=False, band_out=False) -> dict:
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
     pointers valid in this process (own, or mapped with mandel_ipc_open)."""
     st = mandel_stats()
     o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas, adapt_lo, adapt_hi,
-              0, check_every, tile_rows, no_pack)
+              0, check_every, tile_rows, no_pack, band_out)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
                                   _ptr(out_root), _ptr(fcfs_counter), stream, ctypes.byref(st))
@@ -295,6 +301,23 @@ def mandel_plan_rows(scheme, H: int, ngpus: int, rank: int) -> np.ndarray:
                               rows.ctypes.data if cnt.value else None, ctypes.byref(cnt)),
            "mandel_plan_rows")
     return rows
+
+
+def mandel_band_rows() -> np.ndarray:
+    """C: mandel_band_rows (image row of each band row of the last band_out render)."""
+    L = lib()
+    cnt = ctypes.c_uint32(0)
+    _check(L.mandel_band_rows(None, ctypes.byref(cnt)), "mandel_band_rows")
+    rows = np.zeros(cnt.value, dtype=np.uint32)
+    if cnt.value:
+        _check(L.mandel_band_rows(rows.ctypes.data, ctypes.byref(cnt)), "mandel_band_rows")
+    return rows
+
+
+def mandel_scatter_rows(band_dev, rows_dev, nrows: int, W: int, image_dev, stream=None) -> None:
+    """C: mandel_scatter_rows (K4: image[rows[b]] = band[b], device pointers/tensors)."""
+    _check(lib().mandel_scatter_rows(_ptr(band_dev), _ptr(rows_dev), nrows, W, _ptr(image_dev), stream),
+           "mandel_scatter_rows")
 
 
 def mandel_dev_alloc(device: int, nbytes: int) -> int:

@@ -9,6 +9,8 @@ barriers and the timing reductions -- plumbing, not the data path.
 """
 from __future__ import annotations
 
+import numpy as np
+
 from . import mandel as M
 
 
@@ -113,3 +115,90 @@ class RankRenderer:
         for p in self.owned:
             self.M.mandel_dev_free(p)
         self.owned = []
+
+
+class GatherRenderer(RankRenderer):
+    """The NCCL gather path (the cross-check of the fused peer stores).
+
+    Each rank renders its rows into its own compact band (``band_out``: band row b =
+    the rank's b-th row slot), then rank 0 receives every other rank's band and row
+    list with point-to-point sends (torch.distributed P2P ops -- NCCL on a GPU job;
+    with gloo, the CPU test plumbing, through host copies) and places each band in the
+    image with K4 (``mandel_scatter_rows``), the paper's master "reconstructs the
+    image".  FCFS claims still use rank 0's shared counter.
+    """
+
+    def __init__(self, dist, rank, world, device, args, dtype, stream, lib=None, slots=512,
+                 chunk_rows=16):
+        super().__init__(dist, rank, world, device, args, dtype, stream, lib=lib, slots=slots)
+        import torch
+        W, H = int(args[4]), int(args[5])
+        self.W, self.H = W, H
+        c = max(1, int(chunk_rows))
+        self.cap = -(-H // c) * c  # band rows a rank may need (FCFS: every chunk)
+        self.dev = torch.device("cuda", device)
+        self.band = torch.empty((self.cap, W), dtype=torch.int32, device=self.dev)
+        self.host = dist.get_backend() == "gloo"
+        if rank == 0:
+            self.recv = [torch.empty((self.cap, W), dtype=torch.int32, device=self.dev)
+                         for _ in range(world)]
+
+    def step(self, scheme: str, barrier: bool = False, **kw) -> dict:
+        import torch
+        L, dist = self.M, self.dist
+        if self.nstep and self.nstep % self.slots == 0:
+            dist.barrier()
+            if self.rank == 0:
+                L.mandel_dev_zero(self.ctr, self.slots * self.CTR_BYTES, self.stream)
+            dist.barrier()
+        st = L.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world,
+                                  self.band.data_ptr(), self.counter(self.nstep), self.stream,
+                                  band_out=True, **kw)
+        self.nstep += 1
+        rows = torch.from_numpy(L.mandel_band_rows().view(np.int32))
+        cdev = torch.device("cpu") if self.host else self.dev
+        n = torch.tensor([rows.numel()], dtype=torch.int64, device=cdev)
+        counts = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(self.world)]
+        dist.all_gather(counts, n)
+        counts = [int(x.item()) for x in counts]
+        W = self.W
+        if self.rank == 0:
+            bands = {0: (self.band, rows)}
+            ops, recv_rows = [], {}
+            for r in range(1, self.world):
+                if counts[r] == 0:
+                    continue
+                rr = torch.empty(counts[r], dtype=torch.int32, device=cdev)
+                dst = self.recv[r][:counts[r]] if not self.host else \
+                    torch.empty((counts[r], W), dtype=torch.int32)
+                ops += [dist.P2POp(dist.irecv, rr, r), dist.P2POp(dist.irecv, dst, r)]
+                recv_rows[r] = (dst, rr)
+            for w in (dist.batch_isend_irecv(ops) if ops else []):
+                w.wait()
+            for r, (dst, rr) in recv_rows.items():
+                if self.host:
+                    self.recv[r][:counts[r]].copy_(dst)
+                    dst = self.recv[r][:counts[r]]
+                bands[r] = (dst, rr)
+            scatters = 0
+            for r, (b, rw) in bands.items():
+                if counts[r] == 0:
+                    continue
+                rd = rw.to(self.dev)
+                L.mandel_scatter_rows(b.data_ptr(), rd.data_ptr(), counts[r], W, self.img, self.stream)
+                scatters += 1
+            torch.cuda.current_stream(self.dev).synchronize()
+        elif counts[self.rank]:
+            cnt = counts[self.rank]
+            payload = self.band[:cnt] if not self.host else self.band[:cnt].cpu()
+            rsend = rows if self.host else rows.to(self.dev)
+            ops = [dist.P2POp(dist.isend, rsend, 0), dist.P2POp(dist.isend, payload, 0)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if barrier:
+            dist.barrier()
+        st = dict(st)
+        st["band_rows"] = counts[self.rank]
+        if self.rank == 0:
+            st["kernel_launches"] = st["kernel_launches"] + scatters  # K4 launches
+        return st

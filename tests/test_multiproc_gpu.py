@@ -27,7 +27,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, cfg, schemes, q):
+def _worker(rank, world, port, cfg, schemes, q, gather="fused"):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -35,13 +35,14 @@ def _worker(rank, world, port, cfg, schemes, q):
 
     import bench
     from paper_2007_00745_b200 import mandel as M
-    from paper_2007_00745_b200.multiproc import RankRenderer, aggregate
+    from paper_2007_00745_b200.multiproc import GatherRenderer, RankRenderer, aggregate
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         stream = torch.cuda.current_stream(0).cuda_stream
-        rr = RankRenderer(dist, rank, world, 0, cfg.args(), cfg.dtype, stream, slots=4)
+        cls = GatherRenderer if gather == "nccl" else RankRenderer
+        rr = cls(dist, rank, world, 0, cfg.args(), cfg.dtype, stream, slots=4)
         res = {}
         for scheme in schemes:
             for rep in range(3):  # several renders: counter slots are used in turn and recycled
@@ -64,16 +65,18 @@ def _worker(rank, world, port, cfg, schemes, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("gather", ["fused", "nccl"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("dtype", ["fp64", "fp32"])
-def test_rank_processes_share_one_map(oracle, world, dtype):
+def test_rank_processes_share_one_map(oracle, world, dtype, gather):
     cfg = wl.C1.with_(dtype=dtype, W=517, H=389, iter_max=1500)
     want = oracle.render(cfg)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     schemes = ("fcfs", "cyclic", "block")
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, schemes, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, schemes, q, gather))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
@@ -86,3 +89,45 @@ def test_rank_processes_share_one_map(oracle, world, dtype):
         bad = int((img != want).sum())
         assert bad == 0, f"{scheme} step {rep}: {bad} pixels differ from the oracle"
         assert iters == int(want.sum(dtype=np.uint64)), (scheme, rep)
+
+
+@pytest.mark.parametrize("scheme", ["block", "cyclic", "fcfs", "fcfs_master"])
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+def test_band_mode_and_scatter(mandel, oracle, scheme, nranks):
+    """The NCCL path's device pieces in one process: each rank renders its compact band
+    (band_out), mandel_band_rows lists the band's image rows, K4 places it."""
+    import torch
+    cfg = wl.C1.with_(W=301, H=203, iter_max=800)
+    want = oracle.render(cfg)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    image = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
+    ctr = torch.zeros(64, dtype=torch.int32, device=dev)
+    cap = -(-cfg.H // 16) * 16
+    chunk = 1 if scheme == "fcfs_master" else 16
+    cap = -(-cfg.H // chunk) * chunk
+    seen = []
+    for r in range(nranks):
+        band = torch.full((cap, cfg.W), -7, dtype=torch.int32, device=dev)
+        st = mandel.mandel_render_rank(*cfg.args(), "fp64", scheme, r, nranks, band, ctr, stream,
+                                       band_out=True)
+        rows = mandel.mandel_band_rows()
+        if scheme in ("block", "cyclic"):
+            assert rows.tolist() == mandel.mandel_plan_rows(scheme, cfg.H, nranks, r).tolist()
+        valid = rows[rows != 0xFFFFFFFF]
+        seen += valid.tolist()
+        assert st["rank_rows"][0] == len(valid)
+        # written band rows hold the oracle's rows; unused slots were never written
+        got = band[: len(rows)].cpu().numpy().view(np.uint32)
+        for b, row in enumerate(rows.tolist()):
+            if row != 0xFFFFFFFF:
+                assert np.array_equal(got[b], want[row]), (scheme, r, b, row)
+            else:
+                assert (got[b] == np.uint32(0xFFFFFFF9)).all()
+        if len(rows):
+            rd = torch.from_numpy(rows.view(np.int32)).to(dev)
+            mandel.mandel_scatter_rows(band, rd, len(rows), cfg.W, image, stream)
+    torch.cuda.synchronize()
+    assert sorted(seen) == list(range(cfg.H))
+    got = image.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want)
