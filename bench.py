@@ -425,13 +425,15 @@ def cpu_baseline(cfg, cpu_seconds, gpu_img=None):
     rows = cpu_sample_rows(cfg, cpu_seconds, cores)
     oracle.lib()
     t0 = time.perf_counter()
-    ref, used = oracle.render_rows_mt(cfg, rows, threads=cores)
+    # FCFS chunks small enough that every host thread gets work on a short sample
+    chunk = max(1, min(16, len(rows) // (8 * cores)))
+    ref, used = oracle.render_rows_mt(cfg, rows, threads=cores, chunk=chunk)
     dt = time.perf_counter() - t0
     iters = int(ref.sum(dtype=np.uint64))
     out = {"value": round(iters / dt / 1e9, 4), "unit": "Giter/s", "cores": used, "kind": "oracle",
            "sample": f"{len(rows)} evenly strided rows of {cfg.name} ({len(rows)}/{cfg.H} rows, "
                      f"{iters} pixel-iterations), plain C oracle (-O2 -ffp-contract=off) on "
-                     f"{used} host threads claiming 16-row chunks", "seconds": round(dt, 3),
+                     f"{used} host threads claiming {chunk}-row chunks", "seconds": round(dt, 3),
            "per_core": round(iters / dt / 1e9 / used, 5)}
     if gpu_img is not None:
         got = gpu_img[rows.tolist()].cpu().numpy().view(np.uint32)
