@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 4
+#define MANDEL_ABI_VERSION 5
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -142,6 +142,8 @@ typedef struct mandel_options {
     int      adapt_hi;       /* ADAPTIVE: lazy runs before probing eager again; 0 -> default         */
     int      bands;          /* one GPU + out_host: row bands whose device->host copies overlap
                                 the later bands' compute (0 -> 8, 1 -> no pipelining, max 32)     */
+    int      band_taper;     /* pipelined bands: band pair p (outside-in) holds a share taper^p
+                                of the rows, in percent (100 = equal bands); 0 -> 70            */
     int      tile_rows;      /* persistent kernels: row slots per warp tile (power of two <= 64;
                                 a tile is tile_rows x tile_px/tile_rows pixels, handed to the
                                 warp in 8-column blocks); FCFS cuts it to divide chunk_rows;

@@ -177,6 +177,7 @@ struct Root {
     size_t band_state_bytes = 0;
     cudaStream_t band_stream = nullptr, copy_stream = nullptr;
     cudaEvent_t band_k0[kMaxBands] = {}, band_k1[kMaxBands] = {}, band_cp[kMaxBands] = {};
+    cudaEvent_t copy_done = nullptr;
 };
 
 std::mutex g_mu;
@@ -293,6 +294,7 @@ constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 3, 8},    /
                                             {MANDEL_KERNEL_EAGER, 2, 3, 8}};   // fp64 FMA
 constexpr uint32_t kDefaultRefillLanes = 16;  // LAZY on C4: 8 -> 1509, 16 -> 1555 Giter/s
 constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
+constexpr double kDefaultBandTaper = 0.7;  // band pair p holds a 0.7^p share of the rows
 constexpr int kDefaultBands = 8;  // C2: 4 -> 8.50 ms, 8 -> 8.29 ms, 16 -> 8.86 ms per render (e2e_probe)  // pipelined device->host hand-off (one GPU, host output)
 
 int device_count(int& n) {
@@ -578,6 +580,21 @@ struct ViewKey {
     }
 };
 std::map<ViewKey, KernelChoice> g_auto;
+std::map<ViewKey, float> g_view_ms;  // last compute time of a view (one GPU), for the band split
+
+// Pipelined hand-off shape for a view whose last compute took `ms` (< 0: unknown) and
+// whose map takes ~copy_ms over PCIe: copy-bound views want equal bands (copies start
+// early), compute-bound ones thin late bands (short exposed tail); long renders afford
+// more bands.  Measured (profiles/r01k_e2e_bands.jsonl): C2 8 bands taper 0.4-0.55,
+// C3 (copy-bound) equal bands, C4 (balanced) 12 / 0.7, C5 12-16 / 0.5.
+void band_shape(float ms, double copy_ms, int& bands, double& taper) {
+    bands = kDefaultBands;
+    taper = kDefaultBandTaper;
+    if (ms < 0) return;
+    const double r = ms / copy_ms;
+    taper = r >= 1.15 ? 0.5 : (r <= 0.9 ? 1.0 : 0.7);
+    bands = ms > 10.0 ? 12 : 8;
+}
 float g_probe[2] = {0, 0};  // last probe: eager sample time (ms), eager iterations per exit
 constexpr float kLazyBelowItersPerExit = 10.0f;
 constexpr uint32_t kProbeStride = 16;
@@ -638,7 +655,7 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
 int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                   const mandel_options* opts, uint32_t* image, uint32_t* out_host, void* stream0v,
                   mandel_stats* stats, int bands, size_t sbytes, double t_call,
-                  const KernelChoice* choice) {
+                  const KernelChoice* choice, double taper_auto, float* compute_ms_out) {
     int rc = ensure_rank(0, 0, sbytes, nullptr);
     if (rc) return rc;
     CK(cudaSetDevice(0));
@@ -652,16 +669,35 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
     }
     if (!g_root.band_stream) CK(cudaStreamCreateWithFlags(&g_root.band_stream, cudaStreamDefault));
     if (!g_root.copy_stream) CK(cudaStreamCreateWithFlags(&g_root.copy_stream, cudaStreamDefault));
+    if (!g_root.copy_done) CK(cudaEventCreateWithFlags(&g_root.copy_done, cudaEventDisableTiming));
     for (int b = 0; b < bands; ++b) {
         if (!g_root.band_k0[b]) CK(cudaEventCreate(&g_root.band_k0[b]));
         if (!g_root.band_k1[b]) CK(cudaEventCreate(&g_root.band_k1[b]));
         if (!g_root.band_cp[b]) CK(cudaEventCreate(&g_root.band_cp[b]));
     }
+    // bands in issue order, outside-in (top, bottom, next top, ...): the edges of a view
+    // are usually its cheap rows, so their copies drain while the costly middle still
+    // computes.  Band pair p gets a share taper^p of the rows, so the bands issued last
+    // (the middle, finishing last) are thin and their exposed copies short.
+    const double taper = (opts && opts->band_taper > 0) ? opts->band_taper / 100.0 : taper_auto;
+    std::vector<double> w(bands);
+    double wsum = 0;
+    for (int i = 0; i < bands; ++i) wsum += (w[i] = std::pow(taper, i / 2));
     std::vector<LaunchSpec> specs(bands);
     std::vector<uint32_t> r0(bands), nr(bands);
+    uint32_t top = 0, bot = H;
     for (int b = 0; b < bands; ++b) {
-        r0[b] = (uint32_t)((uint64_t)H * b / bands);
-        nr[b] = (uint32_t)((uint64_t)H * (b + 1) / bands) - r0[b];
+        uint32_t n = (uint32_t)std::llround((double)H * w[b] / wsum);
+        if (b == bands - 1 || n > bot - top) n = bot - top;
+        if (n == 0) n = bot - top > 0 ? 1 : 0;
+        if (b & 1) {
+            bot -= n;
+            r0[b] = bot;
+        } else {
+            r0[b] = top;
+            top += n;
+        }
+        nr[b] = n;
         Plan pl{nr[b], r0[b], 1, nr[b], 0};
         char* st = reinterpret_cast<char*>(g_root.band_state) + sbytes * b;
         rc = build_params(d, W, H, iter_max, dtype, scheme, 1, 0, opts, image, st, sbytes,
@@ -675,25 +711,24 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
     CK(cudaEventRecord(g_root.start, s0));
     CK(cudaStreamWaitEvent(cs[1], g_root.start, 0));
     CK(cudaStreamWaitEvent(cp, g_root.start, 0));
-    // outside-in band order (0, B-1, 1, B-2, ...): the edges of a view are usually the
-    // cheap rows, so their copies drain while the costly middle bands still compute
     for (int i = 0; i < bands; ++i) {
-        const int b = (i & 1) ? bands - 1 - i / 2 : i / 2;
+        const int b = i;
         cudaStream_t s = cs[i & 1];
         CK(cudaEventRecord(g_root.band_k0[b], s));
         rc = launch(specs[b], s);
         if (rc) return rc;
         CK(cudaEventRecord(g_root.band_k1[b], s));
+        if (nr[b] == 0) continue;
         CK(cudaStreamWaitEvent(cp, g_root.band_k1[b], 0));
         const size_t off = (size_t)r0[b] * W;
         CK(cudaMemcpyAsync(out_host + off, image + off, (size_t)nr[b] * W * sizeof(uint32_t),
                            cudaMemcpyDeviceToHost, cp));
         CK(cudaEventRecord(g_root.band_cp[b], cp));
     }
+    CK(cudaEventRecord(g_root.copy_done, cp));  // the copy stream is in order: all copies done
     // s0 (the caller's stream) is done when every band kernel and every copy is
     for (int b = 0; b < bands; ++b) CK(cudaStreamWaitEvent(s0, g_root.band_k1[b], 0));
-    const int last = (bands & 1) ? (bands - 1) / 2 : bands / 2;  // last band issued
-    CK(cudaStreamWaitEvent(s0, g_root.band_cp[last], 0));
+    CK(cudaStreamWaitEvent(s0, g_root.copy_done, 0));
     CK(cudaEventRecord(g_root.d2h, s0));
     std::vector<mandel::WorkState> ws(bands);
     for (int b = 0; b < bands; ++b)
@@ -713,6 +748,7 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
             stats->loop_exits += ws[b].exits;
         }
         stats->device_ms = kend;
+        *compute_ms_out = kend;
         stats->kernel_ms[0] = kend;
         stats->kernel_ms_max = kend;
         CK(cudaEventElapsedTime(&ms, g_root.start, g_root.d2h));
@@ -796,10 +832,23 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     }
     const bool auto_k = !opts || opts->kernel == MANDEL_KERNEL_REFILL;
     const KernelChoice* kcp = auto_k ? &kc : nullptr;
-    const int bands = opts && opts->bands ? opts->bands : kDefaultBands;
-    if (out_host && ngpus == 1 && bands > 1 && H >= 2 * (uint32_t)bands && scheme != MANDEL_FCFS_MASTER)
-        return render_banded(d, W, H, iter_max, dtype, scheme, opts, image, out_host, stream0v,
-                             stats, bands > kMaxBands ? kMaxBands : bands, sbytes, t_call, kcp);
+    const ViewKey vkey{{xmin, xmax, ymin, ymax, R}, W, H, iter_max, dtype};
+    int bands_auto = kDefaultBands;
+    double taper_auto = kDefaultBandTaper;
+    {
+        auto vm = g_view_ms.find(vkey);
+        band_shape(vm == g_view_ms.end() ? -1.f : vm->second, (double)bytes / 5.0e7, bands_auto, taper_auto);
+    }
+    const int bands = opts && opts->bands ? opts->bands : bands_auto;
+    if (out_host && ngpus == 1 && bands > 1 && H >= 2 * (uint32_t)bands && scheme != MANDEL_FCFS_MASTER) {
+        mandel_stats local;
+        float cms = -1.f;
+        rc = render_banded(d, W, H, iter_max, dtype, scheme, opts, image, out_host, stream0v,
+                           stats ? stats : &local, bands > kMaxBands ? kMaxBands : bands, sbytes, t_call,
+                           kcp, taper_auto, &cms);
+        if (rc == MANDEL_OK && cms > 0) g_view_ms[vkey] = cms;
+        return rc;
+    }
     std::vector<LaunchSpec> specs(ngpus);
     for (int r = 0; r < ngpus; ++r) {
         const int dev = r % ndev;
@@ -853,6 +902,11 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         CK(cudaStreamSynchronize(r == 0 ? s0 : rk.stream));
     }
     CK(cudaSetDevice(0));
+    if (ngpus == 1) {
+        float vms = 0;
+        CK(cudaEventElapsedTime(&vms, g_root.start, g_root.done));
+        g_view_ms[vkey] = vms;
+    }
     if (stats) {
         std::memset(stats, 0, sizeof(*stats));
         float ms = 0;
@@ -1233,6 +1287,7 @@ void mandel_shutdown(void) {
         if (g_root.band_state) cudaFree(g_root.band_state);
         if (g_root.band_stream) cudaStreamDestroy(g_root.band_stream);
         if (g_root.copy_stream) cudaStreamDestroy(g_root.copy_stream);
+        if (g_root.copy_done) cudaEventDestroy(g_root.copy_done);
         for (int b = 0; b < kMaxBands; ++b) {
             if (g_root.band_k0[b]) cudaEventDestroy(g_root.band_k0[b]);
             if (g_root.band_k1[b]) cudaEventDestroy(g_root.band_k1[b]);
@@ -1241,6 +1296,7 @@ void mandel_shutdown(void) {
     }
     g_root = Root();
     g_auto.clear();
+    g_view_ms.clear();
     for (auto& d : g_dev) d.init = false;
     cudaGetLastError();
 }

@@ -110,6 +110,7 @@ class mandel_options(ctypes.Structure):
         ("adapt_lo", ctypes.c_int),
         ("adapt_hi", ctypes.c_int),
         ("bands", ctypes.c_int),
+        ("band_taper", ctypes.c_int),
         ("tile_rows", ctypes.c_int),
         ("band_out", ctypes.c_int),
         ("no_pack", ctypes.c_int),
@@ -212,7 +213,7 @@ def _ptr(a) -> int | None:
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
-          tile_rows=0, no_pack=False, band_out=False):
+          tile_rows=0, no_pack=False, band_out=False, band_taper=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -229,6 +230,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.tile_rows = tile_rows or 0
     o.no_pack = 1 if no_pack else 0
     o.band_out = 1 if band_out else 0
+    o.band_taper = band_taper or 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -259,13 +261,13 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      ngpus=1, *, out_host=None, out_dev0=None, stream0=None, chunk_rows=0,
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
-                     bands=0, check_every=0, tile_rows=0, no_pack=False) -> dict:
+                     bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0) -> dict:
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict."""
     st = mandel_stats()
     o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
-              adapt_hi, bands, check_every, tile_rows, no_pack)
+              adapt_hi, bands, check_every, tile_rows, no_pack, False, band_taper)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st))

@@ -20,13 +20,19 @@ t0 = time.perf_counter(); torch.cuda.synchronize()
 host.copy_(dmap, non_blocking=True); torch.cuda.synchronize()
 print(json.dumps({"mode": "plain_d2h_copy_ms", "ms": (time.perf_counter() - t0) * 1e3,
                   "gbs": cfg.W * cfg.H * 4 / (time.perf_counter() - t0) / 1e9}))
-for bands in (1, 4, 8, 16, 32):
-    res = []
-    for _ in range(4):
-        t0 = time.perf_counter()
-        st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, "fcfs", 1, out_host=host, stream0=s,
-                                     bands=bands)
-        res.append(((time.perf_counter() - t0) * 1e3, st["device_ms"], st["d2h_ms"]))
-    best = min(res)
-    print(json.dumps({"mode": "host", "bands": bands, "wall_ms": best[0], "compute_ms": best[1],
-                      "exposed_d2h_ms": best[2]}))
+tapers = [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["100", "70"])]
+blist = [int(v) for v in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["1", "4", "8", "12", "16"])]
+for bands in blist:
+    for taper in tapers:
+        if bands == 1 and taper != tapers[0]:
+            continue
+        res = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, "fcfs", 1, out_host=host, stream0=s,
+                                         bands=bands, band_taper=taper)
+            res.append(((time.perf_counter() - t0) * 1e3, st["device_ms"], st["d2h_ms"]))
+        best = min(res)
+        print(json.dumps({"mode": "host", "config": cfg.name, "bands": bands, "taper": taper,
+                          "wall_ms": round(best[0], 3), "compute_ms": round(best[1], 3),
+                          "exposed_d2h_ms": round(best[2], 3)}), flush=True)
