@@ -208,6 +208,8 @@ def run_ours(args):
         img_ptr = rr.img
         img = None
 
+    shared = None  # N > 1 e2e: the shared host image every rank drains a slice into
+
     def step(scheme, out_host=None, e2e=False):
         if world == 1:
             return mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, 1,
@@ -217,7 +219,12 @@ def run_ours(args):
         # renders follow each other without a barrier (one FCFS counter slot per render);
         # e2e ends each render with one so that rank 0 copies a complete map
         st = rr.step(scheme, barrier=e2e, chunk_rows=args.chunk_rows, kernel=kernel)
-        if out_host is not None and rank == 0:
+        if e2e and shared is not None and shared.ok:
+            # every rank pulls its slice of rank 0's map over NVLink and pushes it through
+            # its own PCIe link into the shared host image; the barrier makes it whole
+            shared.drain(img_ptr, cfg.W, cfg.H, world, s_handle)
+            dist.barrier()
+        elif out_host is not None and rank == 0:
             _d2h(out_host, img_ptr, nbytes, s_handle)  # rank 0 holds the whole map
         return st
 
@@ -324,6 +331,9 @@ def run_ours(args):
         # device->host copy of each step's map inside the timed region
         host = torch.empty((cfg.H, cfg.W), dtype=torch.int32, pin_memory=True) \
             if rank == 0 else None
+        if world > 1:
+            from paper_2007_00745_b200.multiproc import SharedHostImage
+            shared = SharedHostImage(dist, rank, nbytes, _cudart())
         ne = max(1, args.e2e_steps)
         ems, _ = timed(args.scheme, ne, 1, None, out_host=host if rank == 0 else None, e2e=True)
         ems_job, _ = aggregate(dist, ems, 0, adev)
@@ -332,9 +342,18 @@ def run_ours(args):
                        "d2h_bytes_per_step": nbytes, "steps": ne,
                        "note": "inputs are scalar kernel arguments (window, sizes, iterMax, R); "
                                "the map is copied device->host into pinned memory every step"}
+        if world > 1:
+            line["e2e"]["hand_off"] = (
+                f"every rank copies 1/{world} of rank 0's map (NVLink, then its own PCIe link) "
+                "into one shared page-locked host image" if shared.ok else
+                f"rank 0 copies the whole map (shared host image unavailable: {shared.error})")
         if rank == 0 and host is not None:
-            line["e2e"]["map_sum_check"] = int(host.numpy().view(np.uint32).sum(dtype=np.uint64)) \
-                == (iters_rank if world == 1 else iters_job)
+            total = shared.checksum() if (world > 1 and shared.ok) else \
+                int(host.numpy().view(np.uint32).sum(dtype=np.uint64))
+            line["e2e"]["map_sum_check"] = total == (iters_rank if world == 1 else iters_job)
+        if shared is not None:
+            shared.close()
+            shared = None
 
         if not args.no_schemes:
             per = {}

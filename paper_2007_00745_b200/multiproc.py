@@ -202,3 +202,86 @@ class GatherRenderer(RankRenderer):
         if self.rank == 0:
             st["kernel_launches"] = st["kernel_launches"] + scatters  # K4 launches
         return st
+
+
+class SharedHostImage:
+    """The end-to-end destination of a one-process-per-GPU job: one host buffer shared by
+    every rank (POSIX shared memory, page-locked in every process with cudaHostRegister),
+    so that the hand-off of rank 0's map (the master's file write) uses
+    every GPU's PCIe link: rank r copies rows [r*H/N, (r+1)*H/N) of rank 0's map -- over
+    NVLink through its CUDA IPC mapping -- into the shared buffer.  ``ok`` is False when
+    the segment cannot be created or registered; callers then copy from rank 0 alone.
+    """
+
+    def __init__(self, dist, rank: int, nbytes: int, cudart):
+        from multiprocessing import shared_memory
+        import ctypes
+        self.dist, self.rank, self.nbytes, self.cudart = dist, rank, nbytes, cudart
+        self.shm, self.ptr, self.ok = None, 0, False
+        err = ""
+        name = None
+        if rank == 0:
+            try:
+                self.shm = shared_memory.SharedMemory(create=True, size=nbytes)
+                name = self.shm.name
+            except Exception as e:  # e.g. /dev/shm too small
+                err = f"shm: {e}"[:120]
+        name = share_bytes(dist, rank, name)
+        if rank != 0 and name is not None:
+            try:
+                self.shm = shared_memory.SharedMemory(name=name)
+            except Exception as e:
+                err = f"shm attach: {e}"[:120]
+        if self.shm is not None:
+            buf = (ctypes.c_char * nbytes).from_buffer(self.shm.buf)
+            self.ptr = ctypes.addressof(buf)
+            del buf
+            rc = cudart.cudaHostRegister(ctypes.c_void_p(self.ptr), ctypes.c_size_t(nbytes), ctypes.c_uint(1))
+            if rc != 0:
+                err = f"cudaHostRegister rc={rc}"
+                self.ptr = 0
+        ok = 1 if (self.ptr and not err) else 0
+        import torch
+        tdev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" \
+            else torch.device("cpu")
+        t = torch.tensor([ok], dtype=torch.int32, device=tdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        self.ok = bool(t.item())
+        self.error = err
+
+    def rows(self, H: int, world: int):
+        """The row range this rank drains."""
+        r0 = H * self.rank // world
+        return r0, H * (self.rank + 1) // world - r0
+
+    def drain(self, img_ptr: int, W: int, H: int, world: int, stream: int) -> None:
+        """Copy this rank's slice of rank 0's map (device pointer valid here) to the host."""
+        import ctypes
+        r0, n = self.rows(H, world)
+        if n == 0:
+            return
+        off = r0 * W * 4
+        rc = self.cudart.cudaMemcpyAsync(ctypes.c_void_p(self.ptr + off), ctypes.c_void_p(img_ptr + off),
+                                         ctypes.c_size_t(n * W * 4), ctypes.c_int(2), ctypes.c_void_p(stream))
+        if rc != 0:
+            raise RuntimeError(f"cudaMemcpyAsync (shared host slice) failed: {rc}")
+        self.cudart.cudaStreamSynchronize(ctypes.c_void_p(stream))
+
+    def checksum(self) -> int:
+        """Sum of the host image as uint32 counts (no buffer export outlives the call)."""
+        a = np.ndarray((self.nbytes // 4,), dtype=np.uint32, buffer=self.shm.buf)
+        total = int(a.sum(dtype=np.uint64))
+        del a
+        return total
+
+    def close(self):
+        import ctypes
+        if self.ptr:
+            self.cudart.cudaHostUnregister(ctypes.c_void_p(self.ptr))
+            self.ptr = 0
+        self.dist.barrier()
+        if self.shm is not None:
+            self.shm.close()
+            if self.rank == 0:
+                self.shm.unlink()
+            self.shm = None

@@ -131,3 +131,61 @@ def test_band_mode_and_scatter(mandel, oracle, scheme, nranks):
     assert sorted(seen) == list(range(cfg.H))
     got = image.cpu().numpy().view(np.uint32)
     assert np.array_equal(got, want)
+
+
+def _shared_worker(rank, world, port, cfg, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    from paper_2007_00745_b200.multiproc import RankRenderer, SharedHostImage
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        stream = torch.cuda.current_stream(0).cuda_stream
+        rr = RankRenderer(dist, rank, world, 0, cfg.args(), cfg.dtype, stream, slots=4)
+        sh = SharedHostImage(dist, rank, cfg.W * cfg.H * 4, bench._cudart())
+        res = {"ok": sh.ok, "err": sh.error}
+        if sh.ok:
+            for scheme in ("fcfs", "cyclic"):
+                rr.step(scheme, barrier=True)
+                sh.drain(rr.img, cfg.W, cfg.H, world, stream)
+                dist.barrier()
+                if rank == 0:
+                    a = np.ndarray((cfg.H, cfg.W), dtype=np.uint32, buffer=sh.shm.buf).copy()
+                    res[scheme] = a
+                dist.barrier()
+        sh.close()
+        rr.close()
+        q.put((rank, res))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shared_host_image_drain(oracle, world):
+    """N > 1 end to end: every rank copies its slice of rank 0's map (through its CUDA IPC
+    mapping) into one shared page-locked host image; the image equals the oracle's map."""
+    cfg = wl.C1.with_(W=389, H=211, iter_max=900)
+    want = oracle.render(cfg)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shared_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0, res
+    got = res[0]
+    assert isinstance(got, dict), got
+    assert got["ok"], got["err"]
+    for scheme in ("fcfs", "cyclic"):
+        assert np.array_equal(got[scheme], want), scheme
