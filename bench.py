@@ -210,7 +210,7 @@ def run_ours(args):
 
     shared = None  # N > 1 e2e: the shared host image every rank drains a slice into
 
-    def step(scheme, out_host=None, e2e=False):
+    def step(scheme, out_host=None, e2e=False, sync=True):
         if world == 1:
             return mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, 1,
                                            out_host=out_host, out_dev0=img_ptr,
@@ -218,7 +218,7 @@ def run_ours(args):
                                            kernel=kernel)
         # renders follow each other without a barrier (one FCFS counter slot per render);
         # e2e ends each render with one so that rank 0 copies a complete map
-        st = rr.step(scheme, barrier=e2e, chunk_rows=args.chunk_rows, kernel=kernel)
+        st = rr.step(scheme, barrier=e2e, sync=sync or e2e, chunk_rows=args.chunk_rows, kernel=kernel)
         if e2e and shared is not None and shared.ok:
             # every rank pulls its slice of rank 0's map over NVLink and pushes it through
             # its own PCIe link into the shared host image; the barrier makes it whole
@@ -239,8 +239,12 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         t0 = time.time()
         e0.record(stream)
-        for _ in range(steps):
-            stats.append(step(scheme, out_host, e2e))
+        for i in range(steps):
+            # N > 1: renders are enqueued back to back (no host round trip between them);
+            # the last one returns the statistics
+            st = step(scheme, out_host, e2e, sync=(world == 1 or i == steps - 1))
+            if st is not None:
+                stats.append(st)
         e1.record(stream)
         if dist is not None:
             dist.barrier()
@@ -321,7 +325,8 @@ def run_ours(args):
             "l2": f"no input reads; each step writes a {nbytes / 2**20:.0f} MiB map "
                   "(> 126 MB L2) -- nothing to flush",
         },
-        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) if world == 1 else
+                        int(args.steps * stats[-1]["kernel_launches"]),  # N > 1: one stats per loop
         "roofline": roof,
         "clocks": clocks,
     }

@@ -215,12 +215,14 @@ int mandel_render_ex(double xmin, double xmax, double ymin, double ymax,
  *                  (rank 0: its own buffer; others: mapped with mandel_ipc_open).
  *   fcfs_counter : DEVICE pointer to a uint32 chunk counter shared by all ranks (rank 0's
  *                  memory, IPC-mapped elsewhere); must be 0 before any rank starts and is
- *                  only used by MANDEL_FCFS (may be NULL otherwise).  The caller resets it
- *                  and separates renders with a barrier.
+ *                  only used by MANDEL_FCFS (may be NULL otherwise).  Every render needs a
+ *                  counter no rank still claims from (a fresh zeroed one, or a barrier).
  *   stream       : nullable cudaStream_t; the rank runs on the stream's device (else on the
  *                  calling thread's current device).
- * The call returns when this rank's rows are stored in the root image.  stats (nullable)
- * receives this rank's kernel_ms / rank_iters[0] / rank_pixels[0] / chunks_claimed.
+ * With stats != NULL (or options.band_out) the call returns when this rank's rows are
+ * stored and stats receives this rank's kernel_ms / rank_iters[0] / rank_pixels[0] /
+ * chunks_claimed.  With stats == NULL the render is only ENQUEUED on the stream (no host
+ * synchronisation): the caller orders later work with the stream.
  * Errors: as mandel_render_ex, plus EINVAL for rank outside [0, nranks) or a NULL out_root,
  * or FCFS with a NULL fcfs_counter.
  */
@@ -248,6 +250,9 @@ int mandel_ipc_close(void *dev_ptr);
  * (nullable = the legacy default stream of the current device) and wait for it.
  * Used to reset the shared FCFS counter between multi-process renders. */
 int mandel_dev_zero(void *dev_ptr, size_t bytes, void *stream);
+/* Wait for everything enqueued on stream (NULL: the whole current device), e.g. after
+ * asynchronous mandel_render_rank calls (stats == NULL). */
+int mandel_sync(void *stream);
 
 /*
  * mandel_plan_rows -- host-only planner of the static schemes (no GPU needed).

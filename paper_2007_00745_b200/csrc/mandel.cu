@@ -1069,9 +1069,10 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     rc = launch(ls, s);
     if (rc) return rc;
     CK(cudaEventRecord(rk.k1, s));
+    const bool band = opts && opts->band_out;
+    if (!stats && !band) return MANDEL_OK;  // asynchronous: enqueued on the stream, not awaited
     mandel::WorkState ws;
     CK(cudaMemcpyAsync(&ws, rk.state, sizeof(ws), cudaMemcpyDeviceToHost, s));
-    const bool band = opts && opts->band_out;
     std::vector<uint32_t> cmap;
     if (band && ls.p.scheme == MANDEL_FCFS) {
         cmap.resize((size_t)ls.p.nchunks + 1);
@@ -1249,6 +1250,12 @@ int mandel_write_ppm(const char* path, const uint8_t* rgb_host, uint32_t W, uint
     ok = (std::fclose(f) == 0) && ok;
     if (!ok) return fail(MANDEL_EIO, std::string("write failed: ") + path);
     if (bytes_written) *bytes_written = (uint64_t)hl + body;
+    return MANDEL_OK;
+}
+
+int mandel_sync(void* stream) {
+    if (stream) CK(cudaStreamSynchronize((cudaStream_t)stream));
+    else CK(cudaDeviceSynchronize());
     return MANDEL_OK;
 }
 

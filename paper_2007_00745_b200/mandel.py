@@ -168,6 +168,8 @@ def lib():
             L.mandel_dev_zero.restype = i32
             L.mandel_ipc_close.argtypes = [vp]
             L.mandel_ipc_close.restype = i32
+            L.mandel_sync.argtypes = [vp]
+            L.mandel_sync.restype = i32
             L.mandel_band_rows.argtypes = [vp, vp]
             L.mandel_band_rows.restype = i32
             L.mandel_scatter_rows.argtypes = [vp, vp, u32, u32, vp, vp]
@@ -279,17 +281,19 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
                        out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
                        kernel=MANDEL_KERNEL_REFILL, refill_lanes=0, ilp=0,
                        min_ctas=0, adapt_lo=0, adapt_hi=0, check_every=0, tile_rows=0,
-                       no_pack=False, band_out=False) -> dict:
+                       no_pack=False, band_out=False, want_stats=True):
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
-    pointers valid in this process (own, or mapped with mandel_ipc_open)."""
-    st = mandel_stats()
+    pointers valid in this process (own, or mapped with mandel_ipc_open).
+    want_stats=False: the render is only enqueued on ``stream``; returns None."""
+    st = mandel_stats() if want_stats else None
     o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas, adapt_lo, adapt_hi,
               0, check_every, tile_rows, no_pack, band_out)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
-                                  _ptr(out_root), _ptr(fcfs_counter), stream, ctypes.byref(st))
+                                  _ptr(out_root), _ptr(fcfs_counter), stream,
+                                  ctypes.byref(st) if st is not None else None)
     _check(rc, "mandel_render_rank")
-    return st.as_dict()
+    return st.as_dict() if st is not None else None
 
 
 def mandel_plan_rows(scheme, H: int, ngpus: int, rank: int) -> np.ndarray:
@@ -330,6 +334,11 @@ def mandel_dev_alloc(device: int, nbytes: int) -> int:
 
 def mandel_dev_free(ptr: int) -> None:
     _check(lib().mandel_dev_free(ptr), "mandel_dev_free")
+
+
+def mandel_sync(stream=None) -> None:
+    """C: mandel_sync (wait for the stream, or the current device when None)."""
+    _check(lib().mandel_sync(stream), "mandel_sync")
 
 
 def mandel_dev_zero(ptr: int, nbytes: int, stream=None) -> None:

@@ -91,18 +91,24 @@ class RankRenderer:
     def counter(self, n: int) -> int:
         return self.ctr + (n % self.slots) * self.CTR_BYTES
 
-    def step(self, scheme: str, barrier: bool = False, **kw) -> dict:
-        """One render into rank 0's map (see the class notes for the protocol)."""
+    def step(self, scheme: str, barrier: bool = False, sync: bool = True, **kw):
+        """One render into rank 0's map (see the class notes for the protocol).
+        sync=False only enqueues the render on the stream and returns None."""
         L = self.M
         if self.nstep and self.nstep % self.slots == 0:  # every counter used once: recycle
+            L.mandel_sync(self.stream)  # earlier renders may still be claiming (sync=False)
             self.dist.barrier()
             if self.rank == 0:
                 L.mandel_dev_zero(self.ctr, self.slots * self.CTR_BYTES, self.stream)
             self.dist.barrier()
+        if not sync:
+            kw["want_stats"] = False
         st = L.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world, self.img,
                                   self.counter(self.nstep), self.stream, **kw)
         self.nstep += 1
         if barrier:
+            if not sync:  # the barrier orders host calls: the render must be finished first
+                L.mandel_sync(self.stream)
             self.dist.barrier()
         return st
 
@@ -147,6 +153,7 @@ class GatherRenderer(RankRenderer):
         import torch
         L, dist = self.M, self.dist
         if self.nstep and self.nstep % self.slots == 0:
+            L.mandel_sync(self.stream)
             dist.barrier()
             if self.rank == 0:
                 L.mandel_dev_zero(self.ctr, self.slots * self.CTR_BYTES, self.stream)

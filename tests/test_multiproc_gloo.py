@@ -74,6 +74,9 @@ class _RecordingLib:
     def mandel_dev_free(self, ptr):
         self.log.append(("free", ptr))
 
+    def mandel_sync(self, stream):
+        self.log.append(("sync",))
+
     def mandel_render_rank(self, *a, **kw):
         self.log.append(("render", a[13], a[12]))  # (counter pointer, image pointer)
         return {}
@@ -109,7 +112,8 @@ def _step_protocol(dist, rank, world):
     want = []
     for n in range(8):
         if n and n % 3 == 0:
-            want += [("barrier",)] + ([("zero", rr.ctr, 3 * B)] if rank == 0 else []) + [("barrier",)]
+            want += [("sync",), ("barrier",)] + ([("zero", rr.ctr, 3 * B)] if rank == 0 else []) + \
+                [("barrier",)]
         want.append(("render", rr.ctr + (n % 3) * B, rr.img))
     want.append(("barrier",))
     ok = ok and steps == want
