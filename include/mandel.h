@@ -198,6 +198,9 @@ int mandel_render(double xmin, double xmax, double ymin, double ymax,
  *   stream0  : nullable cudaStream_t on device 0; rank 0's work (and the D2H copy) is
  *              ordered on it, so a caller can time the call with events on that stream.
  *   opts     : nullable options;  stats : nullable statistics.
+ * With out_host == NULL and stats == NULL the render is only ENQUEUED (the call returns
+ * without waiting; work ordered on stream0 runs after it); otherwise it returns when the
+ * map is in place.
  * Errors as mandel_render; EINVAL also when both outputs are NULL.
  */
 int mandel_render_ex(double xmin, double xmax, double ymin, double ymax,

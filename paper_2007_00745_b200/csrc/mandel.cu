@@ -884,6 +884,8 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     CK(cudaSetDevice(0));
     for (int r = 1; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].k1, 0));
     CK(cudaEventRecord(g_root.done, s0));
+    // device output without statistics: enqueued only (stream0 orders everything after it)
+    if (!stats && !out_host) return MANDEL_OK;
     if (out_host) {
         CK(cudaMemcpyAsync(out_host, image, bytes, cudaMemcpyDeviceToHost, s0));
         CK(cudaEventRecord(g_root.d2h, s0));

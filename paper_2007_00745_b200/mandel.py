@@ -263,18 +263,20 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      ngpus=1, *, out_host=None, out_dev0=None, stream0=None, chunk_rows=0,
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
-                     bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0) -> dict:
+                     bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0,
+                     want_stats=True):
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
-    Returns the call's statistics as a dict."""
-    st = mandel_stats()
+    Returns the call's statistics as a dict; want_stats=False (device output only)
+    enqueues the render on stream0 without waiting and returns None."""
+    st = mandel_stats() if want_stats else None
     o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
               adapt_hi, bands, check_every, tile_rows, no_pack, False, band_taper)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
-                                _ptr(out_dev0), stream0, ctypes.byref(st))
+                                _ptr(out_dev0), stream0, ctypes.byref(st) if st is not None else None)
     _check(rc, "mandel_render_ex")
-    return st.as_dict()
+    return st.as_dict() if st is not None else None
 
 
 def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, rank, nranks,
