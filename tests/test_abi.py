@@ -95,3 +95,18 @@ def test_no_device_means_enodev_not_fallback(mandel):
     with pytest.raises(mandel.MandelError) as e:
         mandel.render(*wl.C1.args())
     assert e.value.code == mandel.MANDEL_ENODEV
+
+
+def test_band_api_host_checks(mandel):
+    # band_out belongs to mandel_render_rank; the band row list is empty before any band render
+    L = mandel.lib()
+    o = mandel._opts(band_out=True)
+    out = np.zeros(wl.C1.pixels, np.uint32)
+    rc = L.mandel_render_ex(*wl.C1.args(), 0, 0, 1, ctypes.byref(o), out.ctypes.data, None, None, None)
+    assert rc == mandel.MANDEL_EINVAL and "band_out" in mandel.last_error()
+    assert mandel.mandel_band_rows().size == 0
+    assert L.mandel_scatter_rows(None, None, 0, 8, None, None) == mandel.MANDEL_OK  # nothing to do
+    assert L.mandel_scatter_rows(None, None, 4, 8, None, None) == mandel.MANDEL_EINVAL
+    cnt = ctypes.c_uint32(0)
+    assert L.mandel_band_rows(None, None) == mandel.MANDEL_EINVAL
+    assert L.mandel_band_rows(None, ctypes.byref(cnt)) == mandel.MANDEL_OK and cnt.value == 0
