@@ -263,7 +263,10 @@ def run_ours(args):
             sampler.mark(t0, t1)
         ms = e0.elapsed_time(e1)
         if ev:
-            stats[-1]["render_ms_mean"] = statistics.mean(a.elapsed_time(b) for a, b in ev)
+            per = [a.elapsed_time(b) for a, b in ev]
+            stats[-1]["render_ms_mean"] = statistics.mean(per)
+            stats[-1]["render_ms_median"] = statistics.median(per)
+            stats[-1]["render_ms_min"] = min(per)
         return ms, stats
 
     sampler = ClockSampler(local)
@@ -318,6 +321,11 @@ def run_ours(args):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
+        # per-render CUDA-event times on rank 0's launching stream (PAPER.md:237 reports
+        # repetitions; median and minimum)
+        "render_ms": {"mean": round(stats[-1]["render_ms_mean"], 4),
+                      "median": round(stats[-1]["render_ms_median"], 4),
+                      "min": round(stats[-1]["render_ms_min"], 4)},
         "higher_is_better": True,
         "scaling": "strong" if world > 1 else "strong",
         "vs_baseline": None,
