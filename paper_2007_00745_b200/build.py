@@ -58,6 +58,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+TOOLS = ["fp_peak", "loop_bench", "fp_latency"]  # FP-pipe micro-benchmarks (tools/*.cu)
+
+
+def build_tools(force: bool = False) -> list:
+    """nvcc the micro-benchmarks the roofline peak and issue model rest on."""
+    procs, outs = [], []
+    for t in TOOLS:
+        src, out = os.path.join(ROOT, "tools", t + ".cu"), os.path.join(ROOT, "tools", t)
+        outs.append(out)
+        if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+            continue
+        procs.append((t, subprocess.Popen([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                                           "-lineinfo", "-fmad=false", "-o", out, src],
+                                          stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    for t, pr in procs:
+        o, e = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(o + e)
+            raise RuntimeError(f"nvcc failed building tools/{t}")
+    return outs
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)
