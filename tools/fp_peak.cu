@@ -39,6 +39,42 @@ __global__ void __launch_bounds__(256) chains(T seed, int iters, T* sink, unsign
     if (threadIdx.x == 0) atomicAdd(cyc, (unsigned long long)(t1 - t0));
 }
 
+// Packed FP32x2 chains (PTX add/mul.rn.f32x2 -> FADD2/FMUL2): 8 packed chains, i.e.
+// 16 fp32 lane-ops per packed instruction pair -- does packing raise the FP32 pipe rate?
+template <int OP>
+__global__ void __launch_bounds__(256) chains_f32x2(int iters, float* sink, unsigned long long* cyc) {
+    unsigned long long a[8];
+    const float k = 1.0000001f;
+    unsigned long long kk;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(kk) : "f"(k), "f"(k));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float v = 1.0f + threadIdx.x + c;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a[c]) : "f"(v), "f"(v + 0.5f));
+    }
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (OP == 0) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(a[c]) : "l"(kk));
+                else asm volatile("mul.rn.f32x2 %0, %0, %1;" : "+l"(a[c]) : "l"(kk));
+            }
+        }
+    }
+    long long t1 = clock64();
+    float s = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a[c]));
+        s += lo + hi;
+    }
+    if (s == -12345.f) sink[0] = s;
+    if (threadIdx.x == 0) atomicAdd(cyc, (unsigned long long)(t1 - t0));
+}
+
 // The escape-loop body without the exit test (bounded: c = 0.25i keeps |z| < 1).
 template <typename T>
 __global__ void __launch_bounds__(256) mandel_body(int iters, T* sink, unsigned long long* cyc) {
@@ -115,6 +151,8 @@ int main() {
     BENCH("dmul", (chains<double, 1>), (1.0, it / 10, dsink, cyc), (1.0, it, dsink, cyc), chain_ops, false);
     BENCH("fadd", (chains<float, 0>), (1.0f, it / 10, fsink, cyc), (1.0f, it, fsink, cyc), chain_ops, false);
     BENCH("fmul", (chains<float, 1>), (1.0f, it / 10, fsink, cyc), (1.0f, it, fsink, cyc), chain_ops, false);
+    BENCH("fadd2_lane_ops", (chains_f32x2<0>), (it / 10, fsink, cyc), (it, fsink, cyc), 2 * chain_ops, false);
+    BENCH("fmul2_lane_ops", (chains_f32x2<1>), (it / 10, fsink, cyc), (it, fsink, cyc), 2 * chain_ops, false);
     BENCH("mandel_body_f64", (mandel_body<double>), (it / 10, dsink, cyc), (it, dsink, cyc), body_ops, false);
     BENCH("mandel_body_f32", (mandel_body<float>), (it / 10, fsink, cyc), (it, fsink, cyc), body_ops, true);
     printf("}\n");
