@@ -130,7 +130,8 @@ typedef struct mandel_stats {
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
 typedef struct mandel_options {
     uint32_t chunk_rows;     /* FCFS rows per claim; 0 -> 16 (BASELINE.json C5)                   */
-    uint32_t tile_px;        /* pixels per warp tile (persistent kernels); 0 -> 256               */
+    uint32_t tile_px;        /* pixels per warp tile (persistent kernels); 0 -> 256, or 128 / 64
+                                when a rank has < 4096 / < 1024 pixels per resident warp        */
     int      kernel;         /* enum mandel_kernel                                                */
     int      logical_ranks;  /* nonzero: allow ngpus > device count, rank g runs on device
                                 g % count on its own stream (tests; ranks never wait on each other) */

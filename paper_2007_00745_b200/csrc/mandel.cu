@@ -363,7 +363,7 @@ int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
     return MANDEL_OK;
 }
 
-constexpr uint32_t kDefaultTile = 256;     // pixels per tile
+constexpr uint32_t kDefaultTile = 256;     // pixels per tile (large views; small ones use less)
 constexpr uint32_t kDefaultTileRows = 8;   // rows per tile: 8 x 32 px, streamed as 8 x 8 blocks
 constexpr uint32_t kDefaultChunk = 16;
 
@@ -439,7 +439,15 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         return fail(MANDEL_EINVAL, "options.tile_rows must be a power of two <= 64");
     if (kscheme == MANDEL_FCFS)
         while (chunk % trows) trows >>= 1;
-    const uint32_t tpx = (o && o->tile_px) ? o->tile_px : kDefaultTile;
+    // default tile: 256 px, smaller when a rank has few pixels per resident warp (the
+    // first tile draw then decides the critical path: C1 800^2 kernel 79 -> 38 us at 64 px)
+    uint32_t tpx = (o && o->tile_px) ? o->tile_px : kDefaultTile;
+    if (!(o && o->tile_px)) {
+        const uint64_t px_rank = (uint64_t)W * H / (uint64_t)(nranks > 0 ? nranks : 1);
+        const uint64_t warps = (uint64_t)(g_dev[device].sms > 0 ? g_dev[device].sms : 148) * 24;
+        const uint64_t per_warp = px_rank / warps;
+        tpx = per_warp >= 4096 ? 256u : (per_warp >= 1024 ? 128u : 64u);
+    }
     uint32_t tile = tpx / trows > 0 ? tpx / trows : 1u;
     if (tile > W) tile = W;
     mandel::Params& p = ls.p;
