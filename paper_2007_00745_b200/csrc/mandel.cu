@@ -601,7 +601,7 @@ void band_shape(float ms, double copy_ms, int& bands, double& taper) {
     if (ms < 0) return;
     const double r = ms / copy_ms;
     taper = r >= 1.15 ? 0.5 : (r <= 0.9 ? 1.0 : 0.7);
-    bands = ms > 10.0 ? 12 : 8;
+    bands = ms > 10.0 ? 12 : (ms < 0.5 ? 1 : 8);  // sub-0.5 ms renders: launches cost more than overlap saves
 }
 float g_probe[2] = {0, 0};  // last probe: eager sample time (ms), eager iterations per exit
 constexpr float kLazyBelowItersPerExit = 10.0f;
