@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 5
+#define MANDEL_ABI_VERSION 6
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -159,6 +159,9 @@ typedef struct mandel_options {
                                 claim every chunk).  mandel_render_ex -> MANDEL_EINVAL            */
     int      no_pack;        /* fp32: nonzero keeps the batched loop scalar (default: packed
                                 FADD2/FMUL2 on slot pairs when ilp >= 2; bit-identical)           */
+    int      max_sms;        /* persistent kernels: run each rank on exactly this many SMs, one
+                                CTA per SM (a rank as a fixed slice of the GPU; ranks sharing a
+                                GPU then never share an SM); 0 -> every SM, full occupancy      */
     int      check_every;    /* EAGER: z-updates per escape test.  1 -> every update (Eq. 2 as
                                 written); 4, 8 or 16 -> batched (R18): |z|^2 is tested
                                 after every 4th/8th/16th update against a threshold just below

@@ -372,6 +372,7 @@ struct LaunchSpec {
     dim3 grid, block;
     KernelFn fn;
     KernelChoice kc;
+    size_t smem = 0;  // dynamic shared memory (only to pin one CTA per SM, options.max_sms)
 };
 
 int occupancy(int device, int fp32, int variant, int ilp, int mi, KernelFn fn, int& occ) {
@@ -439,6 +440,9 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         return fail(MANDEL_EINVAL, "options.tile_rows must be a power of two <= 64");
     if (kscheme == MANDEL_FCFS)
         while (chunk % trows) trows >>= 1;
+    // cyclic slots are stride0 rows apart: keep a tile's rows within ~8 image rows
+    if (!(o && o->tile_rows) && kscheme == MANDEL_CYCLIC && pl.stride0 > 1)
+        while (trows > 1 && trows * pl.stride0 > kDefaultTileRows) trows >>= 1;
     // default tile: 256 px, smaller when a rank has few pixels per resident warp (the
     // first tile draw then decides the critical path: C1 800^2 kernel 79 -> 38 us at 64 px)
     uint32_t tpx = (o && o->tile_px) ? o->tile_px : kDefaultTile;
@@ -536,7 +540,17 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         int occ = 1;
         int rc2 = occupancy(device, fi, kc.variant, kc.ilp, mi, ls.fn, occ);
         if (rc2) return rc2;
-        ls.grid = dim3((unsigned)(occ * dc.sms));
+        // options.max_sms: the rank is a slice of exactly that many SMs (the paper's task
+        // on one core, tools/paper_tables.py): one CTA per SM -- a dynamic shared memory
+        // request above half an SM's keeps any second CTA (this rank's or another's) off
+        if (o && o->max_sms > 0) {
+            int smem_sm = 0;
+            CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+            ls.smem = (size_t)smem_sm / 2 + 1024;
+            ls.grid = dim3((unsigned)std::min(o->max_sms, dc.sms));
+        } else {
+            ls.grid = dim3((unsigned)(occ * dc.sms));
+        }
     } else {
         ls.grid = dim3((W + 31) / 32, (pl.nslots + mandel::kWarpsPerCta - 1) / mandel::kWarpsPerCta);
         if (pl.nslots == 0) ls.grid.y = 1;
@@ -556,7 +570,10 @@ size_t state_bytes_for(int scheme, uint32_t H, const mandel_options* o) {
 }
 
 int launch(const LaunchSpec& ls, cudaStream_t s) {
-    ls.fn<<<ls.grid, ls.block, 0, s>>>(ls.p);
+    if (ls.smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(ls.fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ls.smem));
+    ls.fn<<<ls.grid, ls.block, ls.smem, s>>>(ls.p);
     CK(cudaGetLastError());
     return MANDEL_OK;
 }

@@ -114,6 +114,7 @@ class mandel_options(ctypes.Structure):
         ("tile_rows", ctypes.c_int),
         ("band_out", ctypes.c_int),
         ("no_pack", ctypes.c_int),
+        ("max_sms", ctypes.c_int),
         ("check_every", ctypes.c_int),
     ]
 
@@ -215,7 +216,7 @@ def _ptr(a) -> int | None:
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
-          tile_rows=0, no_pack=False, band_out=False, band_taper=0):
+          tile_rows=0, no_pack=False, band_out=False, band_taper=0, max_sms=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -233,6 +234,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.no_pack = 1 if no_pack else 0
     o.band_out = 1 if band_out else 0
     o.band_taper = band_taper or 0
+    o.max_sms = max_sms or 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -264,14 +266,14 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
                      bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0,
-                     want_stats=True):
+                     max_sms=0, want_stats=True):
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict; want_stats=False (device output only)
     enqueues the render on stream0 without waiting and returns None."""
     st = mandel_stats() if want_stats else None
     o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
-              adapt_hi, bands, check_every, tile_rows, no_pack, False, band_taper)
+              adapt_hi, bands, check_every, tile_rows, no_pack, False, band_taper, max_sms)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st) if st is not None else None)
