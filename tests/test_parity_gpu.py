@@ -354,3 +354,16 @@ def test_c2_schemes_agree(mandel, scheme):
     out, st = _render_dev(mandel, wl.C2, scheme, 8)
     assert bool((ref == out).all())
     assert st["pixels"] == wl.C2.pixels
+
+
+@pytest.mark.parametrize("max_sms", [1, 3, 16])
+@pytest.mark.parametrize("scheme", SCHEMES + ["fcfs_master"])
+def test_max_sms_slices(mandel, oracle, max_sms, scheme):
+    # ranks as fixed GPU slices (one CTA per SM, the paper-table tool's tasks)
+    cfg = wl.C1.with_(W=257, H=131, iter_max=700)
+    want = oracle.render(cfg)
+    for ngpus in (2, 5):
+        out, st = _render_dev(mandel, cfg, scheme, ngpus, max_sms=max_sms,
+                              kernel=["refill", "lazy2"][ngpus % 2])
+        _assert_same(_host(out), want, f"max_sms={max_sms}/{scheme}/N={ngpus}")
+        assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
