@@ -477,6 +477,13 @@ def cpu_baseline(cfg, cpu_seconds, gpu_img=None):
                      f"{iters} pixel-iterations), plain C oracle (-O2 -ffp-contract=off) on "
                      f"{used} host threads claiming {chunk}-row chunks", "seconds": round(dt, 3),
            "per_core": round(iters / dt / 1e9 / used, 5)}
+    # single-threaded rate: every 8th row of the same sample, one thread
+    srows = rows[::8]
+    t0 = time.perf_counter()
+    sref, _ = oracle.render_rows_mt(cfg, srows, threads=1, chunk=1)
+    sdt = time.perf_counter() - t0
+    out["single_thread"] = {"value": round(int(sref.sum(dtype=np.uint64)) / sdt / 1e9, 5), "unit": "Giter/s",
+                            "rows": int(len(srows)), "seconds": round(sdt, 3)}
     if gpu_img is not None:
         got = gpu_img[rows.tolist()].cpu().numpy().view(np.uint32)
         out["parity_rows_vs_gpu"] = {"rows": int(len(rows)), "mismatched_pixels": int((got != ref).sum())}
