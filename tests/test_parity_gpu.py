@@ -266,6 +266,18 @@ def test_host_output_entry_point(mandel, oracle):
     assert st["d2h_ms"] > 0
 
 
+@pytest.mark.parametrize("taper", [0, 30, 70, 100])
+@pytest.mark.parametrize("bands", [2, 5, 12])
+def test_pipelined_band_taper(mandel, oracle, taper, bands):
+    # tapered outside-in bands (thin middle bands) still cover every row exactly once
+    cfg = wl.C1.with_(W=211, H=307, iter_max=500)
+    want = oracle.render(cfg)
+    for rep in range(2):  # the second render uses the view's cached compute time
+        got, st = mandel.render(*cfg.args(), "fp64", "fcfs", 1, bands=bands, band_taper=taper)
+        _assert_same(got, want, f"bands={bands}/taper={taper}/rep={rep}")
+        assert st["sum_iters"] == int(want.sum(dtype=np.uint64)) and st["pixels"] == cfg.pixels
+
+
 @pytest.mark.parametrize("bands", [0, 1, 2, 3, 7, 32])
 @pytest.mark.parametrize("scheme", SCHEMES)
 def test_pipelined_host_output(mandel, oracle, bands, scheme):
