@@ -14,6 +14,14 @@
 // both x2 + y2 and R2 are non-negative and never NaN on a live lane (DESIGN.md
 // "Escape compare"), where integer order equals floating-point order.  That takes
 // the compare off the FP64 pipe (9 -> 8 FP64 instructions per iteration).
+//
+// Kernels: escape_refill_kernel (EAGER: persistent CTAs, 2-D warp tiles, lane refill;
+// the default loop tests |z|^2 every B updates and replays a hit batch exactly,
+// DESIGN.md R18 -- eager_run), escape_lazy_kernel (LAZY: per-update exact escape
+// record, refill when enough lanes are free; the default for incoherent views),
+// escape_adaptive_kernel (switches between the two per warp), escape_static_kernel
+// (one pixel per thread; the A/B baseline).  Arithmetic policies: ArithF64,
+// ArithF64Fma (MANDEL_FP64_FMA, R17), ArithF32, ArithF32P (packed FP32x2 loop).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
