@@ -272,8 +272,10 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
     Returns the call's statistics as a dict; want_stats=False (device output only)
     enqueues the render on stream0 without waiting and returns None."""
     st = mandel_stats() if want_stats else None
-    o = _opts(chunk_rows, tile_px, kernel, logical_ranks, refill_lanes, ilp, min_ctas, adapt_lo,
-              adapt_hi, bands, check_every, tile_rows, no_pack, False, band_taper, max_sms)
+    o = _opts(chunk_rows=chunk_rows, tile_px=tile_px, kernel=kernel, logical_ranks=logical_ranks,
+              refill_lanes=refill_lanes, ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo,
+              adapt_hi=adapt_hi, bands=bands, check_every=check_every, tile_rows=tile_rows,
+              no_pack=no_pack, band_taper=band_taper, max_sms=max_sms)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st) if st is not None else None)
@@ -290,8 +292,9 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
     pointers valid in this process (own, or mapped with mandel_ipc_open).
     want_stats=False: the render is only enqueued on ``stream``; returns None."""
     st = mandel_stats() if want_stats else None
-    o = _opts(chunk_rows, tile_px, kernel, False, refill_lanes, ilp, min_ctas, adapt_lo, adapt_hi,
-              0, check_every, tile_rows, no_pack, band_out)
+    o = _opts(chunk_rows=chunk_rows, tile_px=tile_px, kernel=kernel, refill_lanes=refill_lanes,
+              ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo, adapt_hi=adapt_hi,
+              check_every=check_every, tile_rows=tile_rows, no_pack=no_pack, band_out=band_out)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
                                   _ptr(out_root), _ptr(fcfs_counter), stream,
