@@ -149,7 +149,8 @@ class GatherRenderer(RankRenderer):
             self.recv = [torch.empty((self.cap, W), dtype=torch.int32, device=self.dev)
                          for _ in range(world)]
 
-    def step(self, scheme: str, barrier: bool = False, **kw) -> dict:
+    def step(self, scheme: str, barrier: bool = False, sync: bool = True, **kw) -> dict:
+        """One render + gather (always synchronous: the band's row list is read back)."""
         import torch
         L, dist = self.M, self.dist
         if self.nstep and self.nstep % self.slots == 0:
