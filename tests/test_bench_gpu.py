@@ -48,14 +48,21 @@ def test_bench_single_gpu():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["parity_rows_vs_gpu"]["mismatched_pixels"] == 0
 
 
-@pytest.mark.parametrize("gather", ["fused", "nccl"])
-def test_bench_two_ranks_shared_device(gather):
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29641" if gather == "fused" else "29642",
-                        "bench.py", "--gpus", "2", "--config", "C1", "--steps", "4", "--warmup", "3",
-                        "--e2e-steps", "2", "--no-schemes", "--share-device", "--gather", gather],
-                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+@pytest.mark.parametrize("gather,scheme,schemes", [("fused", "fcfs", False), ("nccl", "fcfs", False),
+                                                   ("fused", "block", True), ("nccl", "cyclic", True)])
+def test_bench_two_ranks_shared_device(gather, scheme, schemes):
+    port = {"fused": 29641, "nccl": 29642}[gather] + (10 if schemes else 0)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           "bench.py", "--gpus", "2", "--config", "C1", "--steps", "4", "--warmup", "3",
+           "--e2e-steps", "2", "--share-device", "--gather", gather, "--scheme", scheme]
+    if not schemes:
+        cmd.append("--no-schemes")
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _line(r.stdout)
     _check_contract(d, 2)
     assert d["test_only_shared_device"] is True
+    if schemes:
+        assert set(d["per_scheme"]) == {"block", "cyclic", "fcfs"}
+        assert all(v["value"] > 0 for v in d["per_scheme"].values())
