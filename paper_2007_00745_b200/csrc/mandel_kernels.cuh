@@ -452,7 +452,11 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
             while (kmax - k >= BT) {
                 T sx[ILP], sy[ILP];
                 bool hit;
-                for (;;) {  // the hot loop: BT updates, one test
+                // the hot loop: BT updates, one test; a down-counter of whole batches is
+                // its only loop state (k is advanced once, after the loop)
+                const uint32_t nb0 = (kmax - k) / BT;
+                uint32_t nb = nb0;
+                for (;;) {
 #pragma unroll
                     for (int s = 0; s < ILP; ++s) {
                         sx[s] = x[s];
@@ -460,9 +464,9 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                     }
                     hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero);
                     if (hit) break;
-                    k += BT;
-                    if (kmax - k < BT) break;
+                    if (--nb == 0) break;
                 }
+                k += (nb0 - nb) * BT;  // batches completed without a hit
                 if (!hit) break;
                 uint32_t ne[ILP], lv[ILP];
 #pragma unroll
