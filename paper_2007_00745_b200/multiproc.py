@@ -62,7 +62,7 @@ class RankRenderer:
     CTR_BYTES = 256
 
     def __init__(self, dist, rank: int, world: int, device: int, args, dtype: str, stream, lib=None,
-                 slots: int = 512):
+                 slots: int = 512, images: int = 1):
         self.M = lib if lib is not None else M
         self.dist, self.rank, self.world, self.device = dist, rank, world, device
         self.args, self.dtype, self.stream = tuple(args), dtype, stream
@@ -73,26 +73,29 @@ class RankRenderer:
         self.mapped = []
         self.nstep = 0
         L = self.M
+        # ``images`` maps on rank 0 (2: a render can proceed while the previous one is
+        # drained to the host, bench.py's pipelined e2e)
         if rank == 0:
-            self.img = L.mandel_dev_alloc(device, self.nbytes)
+            self.imgs = [L.mandel_dev_alloc(device, self.nbytes) for _ in range(images)]
             ctr = L.mandel_dev_alloc(device, slots * self.CTR_BYTES)
             L.mandel_dev_zero(ctr, slots * self.CTR_BYTES, stream)
-            self.owned = [self.img, ctr]
-            handles = (L.mandel_ipc_handle(self.img), L.mandel_ipc_handle(ctr))
+            self.owned = self.imgs + [ctr]
+            handles = tuple(L.mandel_ipc_handle(p) for p in self.imgs) + (L.mandel_ipc_handle(ctr),)
             share_bytes(dist, rank, handles)
         else:
             handles = share_bytes(dist, rank, None)
-            self.img = L.mandel_ipc_open(device, handles[0])
-            ctr = L.mandel_ipc_open(device, handles[1])
-            self.mapped = [self.img, ctr]
+            self.imgs = [L.mandel_ipc_open(device, h) for h in handles[:-1]]
+            ctr = L.mandel_ipc_open(device, handles[-1])
+            self.mapped = self.imgs + [ctr]
+        self.img = self.imgs[0]
         self.ctr = ctr
         dist.barrier()
 
     def counter(self, n: int) -> int:
         return self.ctr + (n % self.slots) * self.CTR_BYTES
 
-    def step(self, scheme: str, barrier: bool = False, sync: bool = True, **kw):
-        """One render into rank 0's map (see the class notes for the protocol).
+    def step(self, scheme: str, barrier: bool = False, sync: bool = True, image: int = 0, **kw):
+        """One render into rank 0's map ``image`` (see the class notes for the protocol).
         sync=False only enqueues the render on the stream and returns None."""
         L = self.M
         if self.nstep and self.nstep % self.slots == 0:  # every counter used once: recycle
@@ -103,7 +106,7 @@ class RankRenderer:
             self.dist.barrier()
         if not sync:
             kw["want_stats"] = False
-        st = L.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world, self.img,
+        st = L.mandel_render_rank(*self.args, self.dtype, scheme, self.rank, self.world, self.imgs[image],
                                   self.counter(self.nstep), self.stream, **kw)
         self.nstep += 1
         if barrier:
@@ -262,8 +265,9 @@ class SharedHostImage:
         r0 = H * self.rank // world
         return r0, H * (self.rank + 1) // world - r0
 
-    def drain(self, img_ptr: int, W: int, H: int, world: int, stream: int) -> None:
-        """Copy this rank's slice of rank 0's map (device pointer valid here) to the host."""
+    def drain(self, img_ptr: int, W: int, H: int, world: int, stream: int, wait: bool = True) -> None:
+        """Copy this rank's slice of rank 0's map (device pointer valid here) to the host
+        on ``stream``; wait=False returns once the copy is enqueued."""
         import ctypes
         r0, n = self.rows(H, world)
         if n == 0:
@@ -273,7 +277,8 @@ class SharedHostImage:
                                          ctypes.c_size_t(n * W * 4), ctypes.c_int(2), ctypes.c_void_p(stream))
         if rc != 0:
             raise RuntimeError(f"cudaMemcpyAsync (shared host slice) failed: {rc}")
-        self.cudart.cudaStreamSynchronize(ctypes.c_void_p(stream))
+        if wait:
+            self.cudart.cudaStreamSynchronize(ctypes.c_void_p(stream))
 
     def checksum(self) -> int:
         """Sum of the host image as uint32 counts (no buffer export outlives the call)."""
