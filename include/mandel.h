@@ -89,7 +89,7 @@ enum mandel_colour { MANDEL_COLOUR_GRAY = 0, MANDEL_COLOUR_CLASSIC = 1 };
 enum mandel_kernel {
     MANDEL_KERNEL_REFILL = 0,  /* default: EAGER, or LAZY when an EAGER render of a strided 1/16
                                   row sample of the view (once per view, cached) leaves its loop
-                                  more often than once per 10 iterations (incoherent escapes)  */
+                                  more often than once per 23 iterations (incoherent escapes)  */
     MANDEL_KERNEL_STATIC = 1,  /* one pixel per thread, static grid (baseline; BLOCK/CYCLIC only)  */
     MANDEL_KERNEL_EAGER = 2,   /* persistent CTAs, warp tile queue, lane refill on every escape   */
     MANDEL_KERNEL_LAZY = 3,    /* the same, refill batched: escapes recorded in-loop, the warp
@@ -120,7 +120,7 @@ typedef struct mandel_stats {
     int32_t  kernel_variant;       /* enum mandel_kernel actually run (EAGER/LAZY/ADAPTIVE/STATIC)   */
     int32_t  kernel_ilp;           /* pixels per lane of that kernel                                */
     float    probe[2];             /* last view probe (MANDEL_KERNEL_REFILL): eager sample time (ms),
-                                      eager iterations per loop exit (< 10 selects LAZY)           */
+                                      eager iterations per loop exit (< 23 selects LAZY)           */
     uint64_t warp_iters;           /* kernel-choice probe only (else 0): loop iterations over warps */
     uint64_t loop_exits;           /* kernel-choice probe only (else 0): loop exits over warps      */
     int32_t  kernel_batch;         /* EAGER: z-updates per escape check actually run (1, 4, 8, 16)  */

@@ -621,7 +621,10 @@ void band_shape(float ms, double copy_ms, int& bands, double& taper) {
     bands = ms > 10.0 ? 12 : (ms < 0.5 ? 1 : 8);  // sub-0.5 ms renders: launches cost more than overlap saves
 }
 float g_probe[2] = {0, 0};  // last probe: eager sample time (ms), eager iterations per exit
-constexpr float kLazyBelowItersPerExit = 10.0f;
+// LAZY below 23 eager iterations per loop exit: calibrated over 44 views with the
+// batched EAGER default (tools/probe_calibrate.py, profiles/r01t_probe_calibration.jsonl);
+// the previous threshold (10, set against the per-update EAGER loop) lost up to 1.7x.
+constexpr float kLazyBelowItersPerExit = 23.0f;
 constexpr uint32_t kProbeStride = 16;
 
 int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, uint32_t iter_max,
