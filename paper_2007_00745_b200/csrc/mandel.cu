@@ -566,7 +566,10 @@ uint32_t single_rank_claims(uint32_t H, const mandel_options* o) {
 size_t state_bytes_for(int scheme, uint32_t H, const mandel_options* o) {
     const uint32_t chunk = effective_chunk(scheme, o);
     const uint64_t nchunks = ((uint64_t)H + chunk - 1) / chunk;
-    return sizeof(mandel::WorkState) + (nchunks + 2) * sizeof(uint32_t);
+    // rounded to 256 B: the pipelined hand-off packs one state per band back to back,
+    // and each WorkState holds 64-bit counters updated with 64-bit atomics
+    const size_t raw = sizeof(mandel::WorkState) + (nchunks + 2) * sizeof(uint32_t);
+    return (raw + 255) & ~(size_t)255;
 }
 
 int launch(const LaunchSpec& ls, cudaStream_t s) {

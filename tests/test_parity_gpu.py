@@ -266,6 +266,17 @@ def test_host_output_entry_point(mandel, oracle):
     assert st["d2h_ms"] > 0
 
 
+@pytest.mark.parametrize("H", [200, 201, 233, 96])
+def test_pipelined_band_state_alignment(mandel, oracle, H):
+    # band states are packed back to back: odd chunk-map lengths must not misalign the
+    # next band's 64-bit counters (H = 200: 13 FCFS chunks)
+    cfg = wl.C1.with_(W=150, H=H, iter_max=300)
+    want = oracle.render(cfg)
+    for scheme in SCHEMES:
+        got, st = mandel.render(*cfg.args(), "fp64", scheme, 1, bands=7)
+        _assert_same(got, want, f"H={H}/{scheme}")
+
+
 @pytest.mark.parametrize("taper", [0, 30, 70, 100])
 @pytest.mark.parametrize("bands", [2, 5, 12])
 def test_pipelined_band_taper(mandel, oracle, taper, bands):
@@ -379,3 +390,48 @@ def test_max_sms_slices(mandel, oracle, max_sms, scheme):
                               kernel=["refill", "lazy2"][ngpus % 2])
         _assert_same(_host(out), want, f"max_sms={max_sms}/{scheme}/N={ngpus}")
         assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
+
+
+def test_concurrent_call_is_ebusy(mandel, oracle):
+    # calls are not reentrant (include/mandel.h): a second call while one runs -> EBUSY
+    import threading
+    big = wl.C2.with_(iter_max=20000)           # ~50 ms of device time per render
+    small = wl.C1.with_(W=64, H=48, iter_max=100)
+    codes, started = [], threading.Event()
+
+    def long_render():
+        out = np.zeros(big.pixels, dtype=np.uint32)
+        started.set()
+        mandel.mandel_render_ex(*big.args(), "fp64", "fcfs", 1, out_host=out)
+
+    seen_busy = False
+    for _ in range(5):
+        t = threading.Thread(target=long_render)
+        started.clear()
+        t.start()
+        started.wait()
+        for _ in range(200):
+            try:
+                got, _ = mandel.render(*small.args(), "fp64", "block", 1)
+                codes.append(0)
+                _assert_same(got, oracle.render(small), "render beside a busy library")
+            except mandel.MandelError as e:
+                assert e.code == mandel.MANDEL_EBUSY
+                seen_busy = True
+                break
+        t.join()
+        if seen_busy:
+            break
+    assert seen_busy
+
+
+def test_shutdown_and_reuse(mandel, oracle):
+    cfg = wl.C1.with_(W=300, H=200)
+    want = oracle.render(cfg)
+    for _ in range(3):
+        got, st = mandel.render(*cfg.args(), "fp64", "fcfs", 1)
+        _assert_same(got, want, "after shutdown")
+        mandel.mandel_shutdown()
+    mandel.mandel_shutdown()  # idempotent
+    out, st = _render_dev(mandel, cfg, "cyclic", 3)
+    _assert_same(_host(out), want, "device output after shutdown")
