@@ -86,6 +86,22 @@ def main():
             continue
         n_cfg += 1
         out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
+        # the host-output path (pipelined bands, tapers) with random options
+        hkw = dict(bands=int(rng.choice([0, 1, 2, 3, 5, 8, 12])), band_taper=int(rng.choice([0, 40, 70, 100])),
+                   tile_rows=int(rng.choice([0, 1, 2, 4, 8, 16])), tile_px=int(rng.choice([0, 32, 64, 100, 256])),
+                   chunk_rows=int(rng.choice([0, 1, 3, 16])))
+        hscheme = ["block", "cyclic", "fcfs"][n_cfg % 3]
+        try:
+            got, _ = mandel.render(*cfg.args(), dtype, hscheme, 1, **hkw)
+            bad = int((got != want).sum())
+            n_maps += 1
+            n_px += got.size
+            n_bad += bad
+            if bad:
+                fails.append({"cfg": cfg.__dict__, "host_output": hkw, "scheme": hscheme, "bad": bad})
+                print(json.dumps(fails[-1]), flush=True)
+        except mandel.MandelError as e:
+            print(json.dumps({"skip": cfg.name, "host_output": hkw, "why": str(e)[:80]}), flush=True)
         for kern in KERNELS[dtype]:
             kw = {}
             if mandel.KERNELS[kern][2:] and cfg.R < 2.0:
