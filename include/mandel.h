@@ -175,7 +175,7 @@ typedef struct mandel_options {
  * mandel_render -- BASELINE.json north_star entry point.
  *   xmin < xmax, ymin < ymax : the complex window (finite doubles)
  *   W, H      : image width (columns, real axis) and height (rows, imaginary axis), >= 1
- *   iterMax   : iteration cap ("iterationMax"), >= 1
+ *   iterMax   : iteration cap ("iterationMax"), 1 <= iterMax <= 2^32 - 2
  *   R         : escape RADIUS (> 0, R*R finite in dtype); escape is |z|^2 > R*R.
  *               The paper's "Escape Radius 400" is R = 20 (R1).
  *   dtype     : enum mandel_dtype
@@ -183,7 +183,7 @@ typedef struct mandel_options {
  *   ngpus     : GPUs 0..ngpus-1 (1 <= ngpus <= device count)
  *   out_u32   : HOST buffer of W*H uint32, row-major, caller-owned (pinned recommended)
  * Returns MANDEL_OK or a negative mandel_status; on error out_u32 is unspecified.
- * EINVAL: W or H == 0; W*H*4 overflows size_t; iterMax == 0; R <= 0 or non-finite or
+ * EINVAL: W or H == 0; W*H*4 overflows size_t; iterMax == 0 or 2^32 - 1; R <= 0 or non-finite or
  *   R*R non-finite (in dtype); any bound non-finite (in dtype); xmin >= xmax or
  *   ymin >= ymax (after rounding, for fp32); dx or dy == 0 in dtype; dtype/scheme out of
  *   range; out_u32 == NULL; BLOCK/CYCLIC with H < ngpus; FCFS_MASTER with ngpus < 2.

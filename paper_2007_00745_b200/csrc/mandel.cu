@@ -60,6 +60,8 @@ int derive(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint3
     if (W == 0 || H == 0) return fail(MANDEL_EINVAL, "W and H must be >= 1");
     if ((uint64_t)W * (uint64_t)H > (uint64_t)(SIZE_MAX / 4)) return fail(MANDEL_EINVAL, "W*H*4 overflows size_t");
     if (iter_max == 0) return fail(MANDEL_EINVAL, "iterMax must be >= 1");
+    // the kernels mark an idle slot with a remaining budget of 0xffffffff
+    if (iter_max == 0xffffffffu) return fail(MANDEL_EINVAL, "iterMax must be < 2^32 - 1");
     if (dtype != MANDEL_FP64 && dtype != MANDEL_FP32 && dtype != MANDEL_FP64_FMA)
         return fail(MANDEL_EINVAL, "dtype out of range");
     if (!std::isfinite(xmin) || !std::isfinite(xmax) || !std::isfinite(ymin) || !std::isfinite(ymax))

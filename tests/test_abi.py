@@ -59,7 +59,7 @@ def _call(mandel, **kw):
 
 
 BAD_ARGS = [
-    dict(W=0), dict(H=0), dict(iter_max=0), dict(R=0.0), dict(R=-1.0), dict(R=math.inf),
+    dict(W=0), dict(H=0), dict(iter_max=0), dict(iter_max=0xFFFFFFFF), dict(R=0.0), dict(R=-1.0), dict(R=math.inf),
     dict(R=1e200), dict(xmin=math.nan), dict(ymax=math.inf), dict(xmin=1.5), dict(ymin=2.0),
     dict(dtype=3), dict(dtype=-1), dict(dtype=2, R=1e200), dict(scheme=4), dict(scheme=3, ngpus=1), dict(H=3, ngpus=4),
     dict(dtype=1, R=1e20), dict(dtype=1, xmin=-1e39), dict(dtype=1, xmin=1.0, xmax=1.0 + 1e-12),

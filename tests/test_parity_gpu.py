@@ -435,3 +435,30 @@ def test_shutdown_and_reuse(mandel, oracle):
     mandel.mandel_shutdown()  # idempotent
     out, st = _render_dev(mandel, cfg, "cyclic", 3)
     _assert_same(_host(out), want, "device output after shutdown")
+
+
+def test_largest_iter_max(mandel, oracle):
+    # iterMax = 2^32 - 2 (the largest accepted): a window outside the set, every pixel
+    # escapes at its first updates, counts exact
+    cfg = wl.Config("far_out", 2.1, 2.9, 2.1, 2.5, 77, 33, 0xFFFFFFFE, 2.0, "fp64")
+    want = oracle.render(cfg)
+    for kernel in ("refill", "lazy2", "refill1", "batch16x2"):
+        out, st = _render_dev(mandel, cfg, "fcfs", 1, kernel=kernel)
+        _assert_same(_host(out), want, f"iterMax 2^32-2/{kernel}")
+
+
+@pytest.mark.slow
+def test_more_than_2_32_pixels(mandel, oracle):
+    # 70000 x 65000 = 4.55e9 pixels (18.2 GB map): 64-bit pixel offsets and counters
+    torch = _torch()
+    cfg = wl.Config("huge", -2.5, 1.5, -2.0, 2.0, 70000, 65000, 6, 2.0, "fp64")
+    out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device="cuda:0")
+    st = mandel.mandel_render_ex(*cfg.args(), "fp64", "fcfs", 1, out_dev0=out)
+    assert st["pixels"] == cfg.pixels
+    assert int(out.min()) >= 1 and int(out.max()) <= cfg.iter_max
+    assert st["sum_iters"] == int(out.to(torch.int64).sum())
+    rows = [0, 1, 32499, 32500, 64998, 64999]
+    want, _ = oracle.render_rows_mt(cfg, np.array(rows))
+    _assert_same(_host(out[rows]), want, "rows of a 4.55e9-pixel map")
+    del out
+    torch.cuda.empty_cache()
