@@ -462,3 +462,15 @@ def test_more_than_2_32_pixels(mandel, oracle):
     _assert_same(_host(out[rows]), want, "rows of a 4.55e9-pixel map")
     del out
     torch.cuda.empty_cache()
+
+
+def test_max_logical_ranks(mandel, oracle):
+    cfg = wl.C1.with_(W=97, H=130, iter_max=400)
+    want = oracle.render(cfg)
+    for scheme in ("fcfs", "cyclic", "block", "fcfs_master"):
+        out, st = _render_dev(mandel, cfg, scheme, mandel.MANDEL_MAX_GPUS)
+        _assert_same(_host(out), want, f"{mandel.MANDEL_MAX_GPUS} ranks/{scheme}")
+        assert st["kernel_launches"] == mandel.MANDEL_MAX_GPUS
+    with pytest.raises(mandel.MandelError) as e:
+        _render_dev(mandel, cfg, "fcfs", mandel.MANDEL_MAX_GPUS + 1)
+    assert e.value.code == mandel.MANDEL_ENODEV
