@@ -58,6 +58,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_debug(out: str = None) -> str:
+    """libmandel_debug.so: the same library with device-side bounds/alignment checks
+    (MANDEL_DEBUG_CHECKS=1); load it with MANDEL_LIB=... to run the tests against it."""
+    out = out or os.path.join(PKG, "libmandel_debug.so")
+    cmd = [nvcc(), *NVCC_FLAGS, "-DMANDEL_DEBUG_CHECKS=1", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           "-o", out, *SOURCES]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libmandel_debug.so")
+    return out
+
+
 TOOLS = ["fp_peak", "loop_bench", "fp_latency"]  # FP-pipe micro-benchmarks (tools/*.cu)
 
 

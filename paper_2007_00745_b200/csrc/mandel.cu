@@ -530,6 +530,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     ls.fn = kernel_fn(packed ? 3 : fi, kc.variant, kc.ilp, mi, kc.bt);
     p.opaque_zero = 0u;
     p.band = (o && o->band_out) ? 1u : 0u;
+    p.out_rows = p.band ? 0u : H;  // a band's capacity is the caller's (not known here)
     if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
     const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;  // (the probe variant is persistent)
     int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;

@@ -28,6 +28,20 @@
 
 namespace mandel {
 
+// Device-side checks for a debug build (-DMANDEL_DEBUG_CHECKS=1; compute-sanitizer is
+// not available on the test pool): a failed check prints and traps the kernel.
+#ifndef MANDEL_DEBUG_CHECKS
+#define MANDEL_DEBUG_CHECKS 0
+#endif
+#define MANDEL_DCHECK(cond)                                                                 \
+    do {                                                                                    \
+        if (MANDEL_DEBUG_CHECKS && !(cond)) {                                               \
+            printf("MANDEL_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+                   __LINE__, blockIdx.x, threadIdx.x);                                      \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+
 #ifndef MANDEL_LAZY_UNROLL
 #define MANDEL_LAZY_UNROLL 16
 #endif
@@ -66,6 +80,7 @@ struct Params {
     uint32_t tile_shift;             // log2(tile_rows * 8)
     uint32_t opaque_zero;            // 0: ArithF32P's contraction barrier (XOR operand)
     uint32_t band;                   // 1: out is this rank's compact band (row = local slot)
+    uint32_t out_rows;               // rows the out buffer holds (debug checks; H for the image)
     // static schemes: slot s -> row s < count0 ? base0 + s*stride0 : base1 + (s - count0)
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
@@ -316,10 +331,12 @@ __device__ __forceinline__ void tile_pixel(const Params& p, const Tile& t, uint3
         dx = w - dy * bw;
     }
     col = t.j0 + (sub << 3) + dx;
+    MANDEL_DCHECK(q < t.nrows * t.cols && dy < t.nrows && col < t.j0 + t.cols && col < p.W);
     const uint32_t sl = t.base + dy;
     row = p.scheme == kSchemeFcfs ? sl
                                   : (sl < p.count0 ? p.base0 + sl * p.stride0 : p.base1 + (sl - p.count0));
     orow = p.band ? t.slot + dy : row;
+    MANDEL_DCHECK(row < p.H && (p.out_rows == 0 || orow < p.out_rows));
 }
 
 // (ck, cg) caches lane 0's last local->global chunk binding, so only the first
@@ -560,6 +577,7 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
 template <typename AR, int ILP, int MINB, int BT = 1, bool LSTATS = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
+    MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     typedef AR A;
     typedef typename AR::T T;
     const unsigned FULL = 0xffffffffu;
@@ -736,6 +754,7 @@ __device__ __forceinline__ void lazy_run(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP],
 template <typename AR, int ILP, int MINB>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_lazy_kernel(const Params p) {
+    MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -860,6 +879,7 @@ escape_lazy_kernel(const Params p) {
 template <typename AR, int ILP, int MINB, int BT = 1>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_adaptive_kernel(const Params p) {
+    MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;

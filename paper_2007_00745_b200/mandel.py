@@ -287,14 +287,15 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
                        out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
                        kernel=MANDEL_KERNEL_REFILL, refill_lanes=0, ilp=0,
                        min_ctas=0, adapt_lo=0, adapt_hi=0, check_every=0, tile_rows=0,
-                       no_pack=False, band_out=False, want_stats=True):
+                       no_pack=False, band_out=False, max_sms=0, want_stats=True):
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
     pointers valid in this process (own, or mapped with mandel_ipc_open).
     want_stats=False: the render is only enqueued on ``stream``; returns None."""
     st = mandel_stats() if want_stats else None
     o = _opts(chunk_rows=chunk_rows, tile_px=tile_px, kernel=kernel, refill_lanes=refill_lanes,
               ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo, adapt_hi=adapt_hi,
-              check_every=check_every, tile_rows=tile_rows, no_pack=no_pack, band_out=band_out)
+              check_every=check_every, tile_rows=tile_rows, no_pack=no_pack, band_out=band_out,
+              max_sms=max_sms)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
                                   _ptr(out_root), _ptr(fcfs_counter), stream,
