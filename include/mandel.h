@@ -162,6 +162,11 @@ typedef struct mandel_options {
     int      max_sms;        /* persistent kernels: run each rank on exactly this many SMs, one
                                 CTA per SM (a rank as a fixed slice of the GPU; ranks sharing a
                                 GPU then never share an SM); 0 -> every SM, full occupancy      */
+    int      async_host;     /* mandel_render_ex with out_host, one GPU, no out_dev0 and no stats:
+                                return once the render and its banded device->host copy are
+                                enqueued; consecutive calls overlap (alternate library maps), and
+                                out_host is complete after mandel_finish().  Do not touch out_host
+                                of an unfinished call.  0 -> synchronous                          */
     int      check_every;    /* EAGER: z-updates per escape test.  1 -> every update (Eq. 2 as
                                 written); 4, 8 or 16 -> batched (R18): |z|^2 is tested
                                 after every 4th/8th/16th update against a threshold just below
@@ -257,6 +262,8 @@ int mandel_ipc_close(void *dev_ptr);
  * (nullable = the legacy default stream of the current device) and wait for it.
  * Used to reset the shared FCFS counter between multi-process renders. */
 int mandel_dev_zero(void *dev_ptr, size_t bytes, void *stream);
+/* Wait until every asynchronous (options.async_host) render's host output is complete. */
+int mandel_finish(void);
 /* Wait for everything enqueued on stream (NULL: the whole current device), e.g. after
  * asynchronous mandel_render_rank calls (stats == NULL). */
 int mandel_sync(void *stream);

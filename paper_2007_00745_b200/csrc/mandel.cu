@@ -180,6 +180,15 @@ struct Root {
     cudaStream_t band_stream = nullptr, copy_stream = nullptr;
     cudaEvent_t band_k0[kMaxBands] = {}, band_k1[kMaxBands] = {}, band_cp[kMaxBands] = {};
     cudaEvent_t copy_done = nullptr;
+    // asynchronous pipelined renders (options.async_host): two library maps and band-state
+    // sets used by alternate calls, a compute stream of their own, and per-set copy events
+    uint32_t* pp_image[2] = {nullptr, nullptr};
+    size_t pp_image_bytes = 0;
+    void* pp_state[2] = {nullptr, nullptr};
+    size_t pp_state_bytes = 0;
+    cudaStream_t async_stream = nullptr;
+    cudaEvent_t entry = nullptr, pp_done[2] = {nullptr, nullptr};
+    int pp_next = 0;
 };
 
 std::mutex g_mu;
@@ -689,12 +698,37 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
 int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                   const mandel_options* opts, uint32_t* image, uint32_t* out_host, void* stream0v,
                   mandel_stats* stats, int bands, size_t sbytes, double t_call,
-                  const KernelChoice* choice, double taper_auto, float* compute_ms_out) {
+                  const KernelChoice* choice, double taper_auto, float* compute_ms_out,
+                  int async_set = -1) {
     int rc = ensure_rank(0, 0, sbytes, nullptr);
     if (rc) return rc;
     CK(cudaSetDevice(0));
     const size_t need = sbytes * (size_t)bands;
-    if (g_root.band_state_bytes < need) {
+    if (async_set >= 0) {
+        // asynchronous: this call's map and band states are set `async_set` of two
+        const size_t bytes = (size_t)W * H * sizeof(uint32_t);
+        if (g_root.pp_image_bytes < bytes || g_root.pp_state_bytes < need) {
+            CK(cudaDeviceSynchronize());  // earlier asynchronous calls may still use them
+            for (int k = 0; k < 2; ++k) {
+                if (g_root.pp_image[k]) CK(cudaFree(g_root.pp_image[k]));
+                if (g_root.pp_state[k]) CK(cudaFree(g_root.pp_state[k]));
+                g_root.pp_image[k] = nullptr;
+                g_root.pp_state[k] = nullptr;
+            }
+            g_root.pp_image_bytes = g_root.pp_state_bytes = 0;
+            for (int k = 0; k < 2; ++k) {
+                CK(cudaMalloc(&g_root.pp_image[k], bytes));
+                CK(cudaMalloc(&g_root.pp_state[k], need));
+            }
+            g_root.pp_image_bytes = bytes;
+            g_root.pp_state_bytes = need;
+        }
+        image = g_root.pp_image[async_set];
+        if (!g_root.async_stream) CK(cudaStreamCreateWithFlags(&g_root.async_stream, cudaStreamNonBlocking));
+        if (!g_root.entry) CK(cudaEventCreateWithFlags(&g_root.entry, cudaEventDisableTiming));
+        for (int k = 0; k < 2; ++k)
+            if (!g_root.pp_done[k]) CK(cudaEventCreateWithFlags(&g_root.pp_done[k], cudaEventDisableTiming));
+    } else if (g_root.band_state_bytes < need) {
         if (g_root.band_state) CK(cudaFree(g_root.band_state));
         g_root.band_state = nullptr;
         g_root.band_state_bytes = 0;
@@ -733,14 +767,42 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         }
         nr[b] = n;
         Plan pl{nr[b], r0[b], 1, nr[b], 0};
-        char* st = reinterpret_cast<char*>(g_root.band_state) + sbytes * b;
+        char* st = reinterpret_cast<char*>(async_set >= 0 ? g_root.pp_state[async_set] : g_root.band_state) +
+                   sbytes * b;
         rc = build_params(d, W, H, iter_max, dtype, scheme, 1, 0, opts, image, st, sbytes,
                           g_root.fcfs_ctr, false, 0, specs[b], &pl, choice);
         if (rc) return rc;
     }
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
-    cudaStream_t cs[2] = {s0, g_root.band_stream};
     cudaStream_t cp = g_root.copy_stream;
+    if (async_set >= 0) {
+        // after the caller's earlier work on stream0, and after the copies of the call
+        // that last used this set's map (two calls ago); stream0 is not made to wait
+        cudaStream_t a0 = g_root.async_stream, a1 = g_root.band_stream;
+        CK(cudaEventRecord(g_root.entry, s0));
+        for (cudaStream_t x : {a0, a1, cp}) {
+            CK(cudaStreamWaitEvent(x, g_root.entry, 0));
+            CK(cudaStreamWaitEvent(x, g_root.pp_done[async_set], 0));
+        }
+        CK(cudaMemsetAsync(g_root.pp_state[async_set], 0, need, a0));
+        CK(cudaEventRecord(g_root.start, a0));
+        CK(cudaStreamWaitEvent(a1, g_root.start, 0));
+        cudaStream_t cs[2] = {a0, a1};
+        for (int b = 0; b < bands; ++b) {
+            cudaStream_t x = cs[b & 1];
+            rc = launch(specs[b], x);
+            if (rc) return rc;
+            CK(cudaEventRecord(g_root.band_k1[b], x));
+            if (nr[b] == 0) continue;
+            CK(cudaStreamWaitEvent(cp, g_root.band_k1[b], 0));
+            const size_t off = (size_t)r0[b] * W;
+            CK(cudaMemcpyAsync(out_host + off, image + off, (size_t)nr[b] * W * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, cp));
+        }
+        CK(cudaEventRecord(g_root.pp_done[async_set], cp));  // copies are in order on cp
+        return MANDEL_OK;
+    }
+    cudaStream_t cs[2] = {s0, g_root.band_stream};
     CK(cudaMemsetAsync(g_root.band_state, 0, need, s0));
     CK(cudaEventRecord(g_root.start, s0));
     CK(cudaStreamWaitEvent(cs[1], g_root.start, 0));
@@ -874,6 +936,16 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         band_shape(vm == g_view_ms.end() ? -1.f : vm->second, (double)bytes / 5.0e7, bands_auto, taper_auto);
     }
     const int bands = opts && opts->bands ? opts->bands : bands_auto;
+    if (opts && opts->async_host) {
+        // asynchronous pipelined host output (one GPU, library-owned maps, no statistics)
+        if (!out_host || out_dev0 || stats || ngpus != 1 || scheme == MANDEL_FCFS_MASTER)
+            return fail(MANDEL_EINVAL, "async_host needs out_host, no out_dev0, no stats, one GPU");
+        const int nb = std::max(1, std::min(bands, std::min((int)kMaxBands, (int)(H / 2 > 0 ? H / 2 : 1))));
+        const int set = g_root.pp_next;
+        g_root.pp_next ^= 1;
+        return render_banded(d, W, H, iter_max, dtype, scheme, opts, image, out_host, stream0v, nullptr, nb,
+                             sbytes, t_call, kcp, taper_auto, nullptr, set);
+    }
     if (out_host && ngpus == 1 && bands > 1 && H >= 2 * (uint32_t)bands && scheme != MANDEL_FCFS_MASTER) {
         mandel_stats local;
         float cms = -1.f;
@@ -1289,6 +1361,21 @@ int mandel_write_ppm(const char* path, const uint8_t* rgb_host, uint32_t W, uint
     return MANDEL_OK;
 }
 
+int mandel_finish(void) {
+    BusyGuard busy;
+    if (!busy.ok) return fail(MANDEL_EBUSY, "another mandel call is in progress");
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_dev.empty()) return MANDEL_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CK(cudaSetDevice(0));
+    if (g_root.copy_stream) CK(cudaStreamSynchronize(g_root.copy_stream));
+    if (g_root.async_stream) CK(cudaStreamSynchronize(g_root.async_stream));
+    if (g_root.band_stream) CK(cudaStreamSynchronize(g_root.band_stream));
+    cudaSetDevice(prev);
+    return MANDEL_OK;
+}
+
 int mandel_sync(void* stream) {
     if (stream) CK(cudaStreamSynchronize((cudaStream_t)stream));
     else CK(cudaDeviceSynchronize());
@@ -1331,6 +1418,14 @@ void mandel_shutdown(void) {
         if (g_root.band_stream) cudaStreamDestroy(g_root.band_stream);
         if (g_root.copy_stream) cudaStreamDestroy(g_root.copy_stream);
         if (g_root.copy_done) cudaEventDestroy(g_root.copy_done);
+        cudaDeviceSynchronize();  // asynchronous renders may still be in flight
+        for (int k = 0; k < 2; ++k) {
+            if (g_root.pp_image[k]) cudaFree(g_root.pp_image[k]);
+            if (g_root.pp_state[k]) cudaFree(g_root.pp_state[k]);
+            if (g_root.pp_done[k]) cudaEventDestroy(g_root.pp_done[k]);
+        }
+        if (g_root.entry) cudaEventDestroy(g_root.entry);
+        if (g_root.async_stream) cudaStreamDestroy(g_root.async_stream);
         for (int b = 0; b < kMaxBands; ++b) {
             if (g_root.band_k0[b]) cudaEventDestroy(g_root.band_k0[b]);
             if (g_root.band_k1[b]) cudaEventDestroy(g_root.band_k1[b]);

@@ -115,6 +115,7 @@ class mandel_options(ctypes.Structure):
         ("band_out", ctypes.c_int),
         ("no_pack", ctypes.c_int),
         ("max_sms", ctypes.c_int),
+        ("async_host", ctypes.c_int),
         ("check_every", ctypes.c_int),
     ]
 
@@ -169,6 +170,8 @@ def lib():
             L.mandel_dev_zero.restype = i32
             L.mandel_ipc_close.argtypes = [vp]
             L.mandel_ipc_close.restype = i32
+            L.mandel_finish.argtypes = []
+            L.mandel_finish.restype = i32
             L.mandel_sync.argtypes = [vp]
             L.mandel_sync.restype = i32
             L.mandel_band_rows.argtypes = [vp, vp]
@@ -216,7 +219,7 @@ def _ptr(a) -> int | None:
 
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
-          tile_rows=0, no_pack=False, band_out=False, band_taper=0, max_sms=0):
+          tile_rows=0, no_pack=False, band_out=False, band_taper=0, max_sms=0, async_host=False):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -235,6 +238,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.band_out = 1 if band_out else 0
     o.band_taper = band_taper or 0
     o.max_sms = max_sms or 0
+    o.async_host = 1 if async_host else 0
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -266,7 +270,7 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
                      bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0,
-                     max_sms=0, want_stats=True):
+                     max_sms=0, async_host=False, want_stats=True):
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict; want_stats=False (device output only)
@@ -275,7 +279,7 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
     o = _opts(chunk_rows=chunk_rows, tile_px=tile_px, kernel=kernel, logical_ranks=logical_ranks,
               refill_lanes=refill_lanes, ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo,
               adapt_hi=adapt_hi, bands=bands, check_every=check_every, tile_rows=tile_rows,
-              no_pack=no_pack, band_taper=band_taper, max_sms=max_sms)
+              no_pack=no_pack, band_taper=band_taper, max_sms=max_sms, async_host=async_host)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
                                 _ptr(out_dev0), stream0, ctypes.byref(st) if st is not None else None)
@@ -342,6 +346,11 @@ def mandel_dev_alloc(device: int, nbytes: int) -> int:
 
 def mandel_dev_free(ptr: int) -> None:
     _check(lib().mandel_dev_free(ptr), "mandel_dev_free")
+
+
+def mandel_finish() -> None:
+    """C: mandel_finish (every asynchronous render's host output complete)."""
+    _check(lib().mandel_finish(), "mandel_finish")
 
 
 def mandel_sync(stream=None) -> None:

@@ -475,3 +475,45 @@ def test_max_logical_ranks(mandel, oracle):
     with pytest.raises(mandel.MandelError) as e:
         _render_dev(mandel, cfg, "fcfs", mandel.MANDEL_MAX_GPUS + 1)
     assert e.value.code == mandel.MANDEL_ENODEV
+
+
+def test_async_host_pipeline(mandel, oracle):
+    # options.async_host: calls return once enqueued, consecutive renders overlap
+    # (alternate library maps); every host buffer is complete after mandel_finish
+    views = [wl.C1.with_(W=301, H=211, iter_max=600), wl.C1.with_(W=128, H=96, iter_max=2000, dtype="fp32"),
+             wl.Config("zoom", -0.7437, -0.7435, 0.1317, 0.1319, 160, 120, 3000, 2.0, "fp64"),
+             wl.C1.with_(W=301, H=211, iter_max=600)]
+    outs = [np.zeros((v.H, v.W), np.uint32) for v in views]
+    for v, o in zip(views, outs):
+        r = mandel.mandel_render_ex(*v.args(), v.dtype, "fcfs", 1, out_host=o, async_host=True,
+                                    want_stats=False, bands=[0, 3, 1, 5][len(v.name) % 4])
+        assert r is None
+    # a synchronous call in between is ordered with the asynchronous ones
+    got, _ = mandel.render(*views[0].args(), "fp64", "cyclic", 1)
+    _assert_same(got, oracle.render(views[0]), "sync between async")
+    mandel.mandel_finish()
+    for v, o in zip(views, outs):
+        _assert_same(o, oracle.render(v), f"async {v.name}/{v.dtype}")
+    # one host buffer reused by a stream of renders of one view
+    v = views[0]
+    o = np.zeros((v.H, v.W), np.uint32)
+    for _ in range(6):
+        mandel.mandel_render_ex(*v.args(), "fp64", "fcfs", 1, out_host=o, async_host=True, want_stats=False)
+    mandel.mandel_finish()
+    _assert_same(o, oracle.render(v), "async reuse")
+
+
+def test_async_host_rejects_misuse(mandel):
+    torch = _torch()
+    v = wl.C1.with_(W=64, H=64)
+    o = np.zeros((v.H, v.W), np.uint32)
+    with pytest.raises(mandel.MandelError):  # statistics need a synchronous call
+        mandel.mandel_render_ex(*v.args(), "fp64", "fcfs", 1, out_host=o, async_host=True)
+    d = torch.zeros((v.H, v.W), dtype=torch.int32, device="cuda:0")
+    with pytest.raises(mandel.MandelError):  # library-owned maps only
+        mandel.mandel_render_ex(*v.args(), "fp64", "fcfs", 1, out_host=o, out_dev0=d, async_host=True,
+                                want_stats=False)
+    with pytest.raises(mandel.MandelError):
+        mandel.mandel_render_ex(*v.args(), "fp64", "fcfs", 2, out_host=o, async_host=True, want_stats=False,
+                                logical_ranks=True)
+    mandel.mandel_finish()
