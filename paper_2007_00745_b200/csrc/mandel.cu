@@ -940,11 +940,16 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         // asynchronous pipelined host output (one GPU, library-owned maps, no statistics)
         if (!out_host || out_dev0 || stats || ngpus != 1 || scheme == MANDEL_FCFS_MASTER)
             return fail(MANDEL_EINVAL, "async_host needs out_host, no out_dev0, no stats, one GPU");
-        const int nb = std::max(1, std::min(bands, std::min((int)kMaxBands, (int)(H / 2 > 0 ? H / 2 : 1))));
+        // frames overlap each other, so the bands only need to start the copies early:
+        // four equal bands (tools/async_bands.py: C2 5.84, C3 4.68, C4 22.0 ms per frame
+        // against 5.83 / 4.77 / 22.6 with the synchronous shape), one for tiny renders
+        int want = opts->bands ? opts->bands : (bands_auto == 1 ? 1 : 4);
+        const double taper = opts->band_taper ? taper_auto : 1.0;
+        const int nb = std::max(1, std::min(want, std::min((int)kMaxBands, (int)(H / 2 > 0 ? H / 2 : 1))));
         const int set = g_root.pp_next;
         g_root.pp_next ^= 1;
         return render_banded(d, W, H, iter_max, dtype, scheme, opts, image, out_host, stream0v, nullptr, nb,
-                             sbytes, t_call, kcp, taper_auto, nullptr, set);
+                             sbytes, t_call, kcp, taper, nullptr, set);
     }
     if (out_host && ngpus == 1 && bands > 1 && H >= 2 * (uint32_t)bands && scheme != MANDEL_FCFS_MASTER) {
         mandel_stats local;
