@@ -92,7 +92,13 @@ def main():
                    chunk_rows=int(rng.choice([0, 1, 3, 16])))
         hscheme = ["block", "cyclic", "fcfs"][n_cfg % 3]
         try:
-            got, _ = mandel.render(*cfg.args(), dtype, hscheme, 1, **hkw)
+            if n_cfg % 2:  # asynchronous pipelined host output (finished right away)
+                got = np.zeros((cfg.H, cfg.W), np.uint32)
+                mandel.mandel_render_ex(*cfg.args(), dtype, hscheme, 1, out_host=got, async_host=True,
+                                        want_stats=False, **hkw)
+                mandel.mandel_finish()
+            else:
+                got, _ = mandel.render(*cfg.args(), dtype, hscheme, 1, **hkw)
             bad = int((got != want).sum())
             n_maps += 1
             n_px += got.size
