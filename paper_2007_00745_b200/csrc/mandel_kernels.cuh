@@ -127,6 +127,17 @@ struct ArithF64 {
         y2 = mul(y, y);
     }
     static __device__ __forceinline__ double sumsq(double, double, double x2, double y2) { return add(x2, y2); }
+    // step() with x + x supplied (the batched loop keeps it: x = t * 0.5 exactly restores x)
+    static __device__ __forceinline__ void step_t(double t, double& x, double& y, double& x2, double& y2,
+                                                  double cr, double ci) {
+        const double ny = add(mul(t, y), ci);
+        const double nx = add(sub(x2, y2), cr);
+        x = nx;
+        y = ny;
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
+    static __device__ __forceinline__ double half(double t) { return mul(t, 0.5); }
     // the carried squares of a restored z (what step() left next to it)
     static __device__ __forceinline__ void resq(double x, double y, double& x2, double& y2) {
         x2 = mul(x, x);
@@ -149,6 +160,15 @@ struct ArithF64Fma : ArithF64 {
         x2 = 0.0;  // not carried (dead)
     }
     static __device__ __forceinline__ double sumsq(double x, double, double, double y2) { return fma(x, x, y2); }
+    static __device__ __forceinline__ void step_t(double t, double& x, double& y, double& x2, double& y2,
+                                                  double cr, double ci) {
+        const double ny = fma(t, y, ci);
+        const double nx = add(fma(x, x, -y2), cr);
+        x = nx;
+        y = ny;
+        y2 = mul(y, y);
+        x2 = 0.0;
+    }
     static __device__ __forceinline__ void resq(double, double y, double& x2, double& y2) {
         x2 = 0.0;
         y2 = mul(y, y);
@@ -179,6 +199,16 @@ struct ArithF32 {
         y2 = mul(y, y);
     }
     static __device__ __forceinline__ float sumsq(float, float, float x2, float y2) { return add(x2, y2); }
+    static __device__ __forceinline__ void step_t(float t, float& x, float& y, float& x2, float& y2, float cr,
+                                                  float ci) {
+        const float ny = add(mul(t, y), ci);
+        const float nx = add(sub(x2, y2), cr);
+        x = nx;
+        y = ny;
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
+    static __device__ __forceinline__ float half(float t) { return mul(t, 0.5f); }
     static __device__ __forceinline__ void resq(float x, float y, float& x2, float& y2) {
         x2 = mul(x, x);
         y2 = mul(y, y);
@@ -412,9 +442,16 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
 template <typename A, int ILP, int BT, typename T>
 __device__ __forceinline__ bool batch_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
                                           const T (&cr)[ILP], const T (&ci)[ILP], uint32_t r2b,
-                                          uint32_t oz) {
+                                          uint32_t oz, const T (&t0)[ILP]) {
 #pragma unroll
     for (int u = 0; u < BT; ++u) {
+        if constexpr (!A::kPacked) {
+            if (u == 0) {  // the first update takes the caller's x + x (kept for the restore)
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) A::step_t(t0[s], x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+                continue;
+            }
+        }
         if constexpr (A::kPacked) {
 #pragma unroll
             for (int s = 0; s + 1 < ILP; s += 2)
@@ -473,13 +510,15 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                 // its only loop state (k is advanced once, after the loop)
                 const uint32_t nb0 = (kmax - k) / BT;
                 uint32_t nb = nb0;
+                T t0[ILP];  // x + x of the batch start: its first update's operand and x's backup
                 for (;;) {
 #pragma unroll
                     for (int s = 0; s < ILP; ++s) {
-                        sx[s] = x[s];
+                        if constexpr (A::kPacked) sx[s] = x[s];
+                        else t0[s] = A::add(x[s], x[s]);
                         sy[s] = y[s];
                     }
-                    hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero);
+                    hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero, t0);
                     if (hit) break;
                     if (--nb == 0) break;
                 }
@@ -488,7 +527,8 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                 uint32_t ne[ILP], lv[ILP];
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
-                    x[s] = sx[s];
+                    if constexpr (A::kPacked) x[s] = sx[s];
+                    else x[s] = A::half(t0[s]);  // (x + x) * 0.5 = x exactly
                     y[s] = sy[s];
                     A::resq(x[s], y[s], x2[s], y2[s]);
                     lv[s] = rem[s] != kIdleRem ? 1u : 0u;
