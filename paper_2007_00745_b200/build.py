@@ -58,17 +58,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
-def build_debug(out: str = None) -> str:
+def build_debug(out: str = None, define: str = "MANDEL_DEBUG_CHECKS=1", name: str = "libmandel_debug.so") -> str:
     """libmandel_debug.so: the same library with device-side bounds/alignment checks
-    (MANDEL_DEBUG_CHECKS=1); load it with MANDEL_LIB=... to run the tests against it."""
-    out = out or os.path.join(PKG, "libmandel_debug.so")
-    cmd = [nvcc(), *NVCC_FLAGS, "-DMANDEL_DEBUG_CHECKS=1", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+    (MANDEL_DEBUG_CHECKS=1); load it with MANDEL_LIB=... to run the tests against it.
+    build_prof() uses it for the LAZY-loop instrumentation (MANDEL_LAZY_PROF=1)."""
+    out = out or os.path.join(PKG, name)
+    cmd = [nvcc(), *NVCC_FLAGS, "-D" + define, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            "-o", out, *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libmandel_debug.so")
+        raise RuntimeError(f"nvcc failed building {name}")
     return out
+
+
+def build_prof(out: str = None) -> str:
+    """libmandel_prof.so: LAZY slot-state counters printed per launch (tools/lazy_prof.py)."""
+    return build_debug(out, "MANDEL_LAZY_PROF=1", "libmandel_prof.so")
 
 
 TOOLS = ["fp_peak", "loop_bench", "fp_latency"]  # FP-pipe micro-benchmarks (tools/*.cu)

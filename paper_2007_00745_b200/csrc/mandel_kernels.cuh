@@ -736,60 +736,53 @@ escape_refill_kernel(const Params p) {
 }
 
 // ---------------------------------------------------------------------------
-// K1/K2 (lazy refill): like escape_refill_kernel, but a slot that escapes does
-// not end the inner loop.  Each slot keeps its own count n (incremented while
-// the slot is live) and a live flag cleared at its escape, so the exact escape
-// iteration is recorded in-loop; the warp leaves the loop only when at least
-// `refill_lanes` lanes hold a finished slot (then all finished slots are retired
-// and refilled at once), or when the earliest iterMax deadline is reached.  This
-// amortises the refill over several finished pixels -- the eager variant leaves
-// the loop on every escape, which dominates where neighbouring counts differ
-// (C4's zoom: one escape every ~4 warp-iterations).
-// Per slot per iteration: 8 FP ops + 2 compare + 1 count + 1 flag update.
+// K1/K2 (lazy refill): like escape_refill_kernel, but a slot that escapes does not
+// end the inner loop.  The warp runs blocks of LU z-updates on all slots with the
+// exact Eq. 2 test after every update; the test only records e[s], the slot's first
+// escaping update in the block -- one 64-bit compare (two ISETPs) and one predicated
+// min per slot-update, no per-update count or live flag.  At the block end each live
+// slot's count advances by e+1 (it escaped: R3 counts the escaping update) or by LU,
+// capped at iterMax, so the count is min(first escape, iterMax) exactly as Eq. 1-2
+// define it: updates past the escape or past iterMax inside the block change nothing.
+// A finished slot stops counting and waits (its z keeps running, unread); the warp
+// leaves the run only when `refill_lanes` lanes hold a finished slot, then retires
+// and refills all of them in one pass over its tile stream.  This amortises the
+// refill over several finished pixels -- the eager variant leaves the loop on every
+// escape, which dominates where neighbouring counts differ (C4's zoom: one escape
+// every ~2 warp-updates).  The block form replaced a per-update `n += live; live &=
+// in` (1.5 more instructions per slot-update): C4 1739 -> 1770 Giter/s
+// (profiles/r01u_sweep_lazy_record.jsonl).
 // ---------------------------------------------------------------------------
-// One z-update of slot s (lazy kernel): count it if the slot was live before it
-// (n counts the escaping update too, reading R3), then clear `lv` on escape.
-#define LAZY_STEP_SLOT(s)                                                  \
-    do {                                                                   \
-        A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);                   \
-        const bool in_ = !(A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2); \
-        n[s] += lv[s];                                                     \
-        lv[s] = in_ ? lv[s] : 0u;                                          \
-    } while (0)
-
-// LU: updates between two exit tests (the lanes-free ballot); the exit is a
-// refill decision only, so testing every LU updates changes no count.  C4 (LAZY,
-// refill_lanes 16): LU 2 -> 1543, 4 -> 1664, 8 -> 1696, 16 -> 1728 Giter/s
-// (profiles/r01g_sweep_lazy_unroll.jsonl).
-template <typename AR, int ILP, bool DRAIN, int LU = MANDEL_LAZY_UNROLL, typename T = typename AR::T>
-__device__ __forceinline__ void lazy_run(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
-                                         const T (&cr)[ILP], const T (&ci)[ILP],
-                                         uint32_t (&n)[ILP], uint32_t (&lv)[ILP],
-                                         typename AR::bits_t r2, uint32_t kmax,
-                                         int max_live_full) {
-    typedef AR A;
-    const unsigned FULL = 0xffffffffu;
-    uint32_t k = 0;
-    for (;;) {
-        if (kmax - k >= LU) {
+// LU: updates between two exit tests; the exit is a refill decision only, so the
+// interval changes no count.  C4 (refill_lanes 16): LU 2 -> 1543, 4 -> 1664,
+// 8 -> 1696, 16 -> 1728 Giter/s (per-update form; profiles/r01g_sweep_lazy_unroll.jsonl).
+template <typename AR, int ILP, int LU, typename T = typename AR::T>
+__device__ __forceinline__ void lazy_block(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
+                                           const T (&cr)[ILP], const T (&ci)[ILP],
+                                           typename AR::bits_t r2, uint32_t (&e)[ILP]) {
 #pragma unroll
-            for (int u = 0; u < LU; ++u) {
+    for (int s = 0; s < ILP; ++s) e[s] = LU;
 #pragma unroll
-                for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
-            }
-            k += LU;
-        } else {
+    for (int u = 0; u < LU; ++u) {
 #pragma unroll
-            for (int s = 0; s < ILP; ++s) LAZY_STEP_SLOT(s);
-            k += 1;
+        for (int s = 0; s < ILP; ++s) {
+            AR::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+            if (AR::bits(AR::sumsq(x[s], y[s], x2[s], y2[s])) > r2) e[s] = min(e[s], (uint32_t)u);
         }
-        uint32_t acc = DRAIN ? 0u : 1u;
-#pragma unroll
-        for (int s = 0; s < ILP; ++s) acc = DRAIN ? (acc | lv[s]) : (acc & lv[s]);
-        const int c = __popc(__ballot_sync(FULL, acc != 0u));
-        if (k == kmax || c <= max_live_full) break;
     }
 }
+
+// Development instrumentation (-DMANDEL_LAZY_PROF=1 -> libmandel_prof.so, read by
+// tools/lazy_prof.py only): slot-updates of the LAZY loop by slot state -- [live,
+// past its escape inside the block, finished or idle] x [filling, draining] -- and the
+// number of runs per mode; printed by the last CTA of a launch.
+#ifndef MANDEL_LAZY_PROF
+#define MANDEL_LAZY_PROF 0
+#endif
+#if MANDEL_LAZY_PROF
+__device__ unsigned long long g_lazy_prof[8];
+__device__ unsigned int g_lazy_prof_done;
+#endif
 
 template <typename AR, int ILP, int MINB>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
@@ -798,25 +791,25 @@ escape_lazy_kernel(const Params p) {
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
+    constexpr uint32_t LU = MANDEL_LAZY_UNROLL;
     const unsigned FULL = 0xffffffffu;
     const uint32_t lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const B r2 = (B)p.r2bits;
     const T xmin = A::xmin(p), ymax = A::ymax(p), dx = A::dx(p), dy = A::dy(p);
     const T zero = T(0);
-    const int max_live_full = 32 - (int)p.refill_lanes;  // exit when >= refill_lanes lanes have a free slot
+    const int refill_at = (int)p.refill_lanes;  // leave the run when this many lanes hold a finished slot
 
     T x[ILP], y[ILP], x2[ILP], y2[ILP], cr[ILP], ci[ILP];
     uint32_t n[ILP];
-    uint32_t lv[ILP];  // 1 while the slot iterates (live), 0 after its escape or when idle
-    bool has[ILP];
+    bool live[ILP];  // the slot's pixel has not finished (its count still advances)
+    bool has[ILP];   // the slot holds a pixel not yet stored (else idle: z = c = 0)
     uint32_t* dst[ILP];
 #pragma unroll
     for (int s = 0; s < ILP; ++s) {
         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
         n[s] = 0;
-        lv[s] = 0;
-        has[s] = false;
+        live[s] = has[s] = false;
         dst[s] = p.out;
     }
     unsigned long long my_iters = 0, my_pix = 0;
@@ -824,15 +817,17 @@ escape_lazy_kernel(const Params p) {
     uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
-    unsigned need[ILP];
-#pragma unroll
-    for (int s = 0; s < ILP; ++s) need[s] = FULL;
+#if MANDEL_LAZY_PROF
+    unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
     for (;;) {
         // ---- refill free slots from the warp's tile stream
+        unsigned need[ILP];
         uint32_t nd = 0, rank[ILP];
 #pragma unroll
         for (int s = 0; s < ILP; ++s) {
+            need[s] = __ballot_sync(FULL, !has[s]);
             rank[s] = nd + __popc(need[s] & lt_mask);
             nd += __popc(need[s]);
         }
@@ -855,46 +850,87 @@ escape_lazy_kernel(const Params p) {
                 if (((need[s] >> lane) & 1u) && rank[s] >= served && rank[s] < served + take) {
                     uint32_t i, j, o;
                     tile_pixel(p, tl, tq + (rank[s] - served), i, j, o);
-                    cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
-                    ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
+                    cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));  // Cx[j] = xmin + j*dx
+                    ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));  // Cy[i] = ymax - i*dy
                     x[s] = y[s] = x2[s] = y2[s] = zero;
                     n[s] = 0;
-                    lv[s] = 1;
-                    has[s] = true;
+                    live[s] = has[s] = true;
                     dst[s] = p.out + ((size_t)o * p.W + j);
                 }
             }
             tq += take;
             served += take;
         }
-        // ---- iterate until enough slots are finished (or a deadline)
         bool any_live = false;
-        uint32_t left = kIdleRem;
 #pragma unroll
-        for (int s = 0; s < ILP; ++s) {
-            any_live |= lv[s] != 0;
-            if (lv[s]) left = min(left, p.iter_max - n[s]);
-        }
-        if (!__any_sync(FULL, any_live)) break;
-        const uint32_t kmax = __reduce_min_sync(FULL, left);
-        if (more) lazy_run<AR, ILP, false>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, max_live_full);
-        else lazy_run<AR, ILP, true>(x, y, x2, y2, cr, ci, n, lv, r2, kmax, 0);
+        for (int s = 0; s < ILP; ++s) any_live |= live[s];
+        if (!__any_sync(FULL, any_live)) break;  // tiles exhausted and every slot retired
+#if MANDEL_LAZY_PROF
+        prof[more ? 6 : 7] += 1;
+#endif
 
-        // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)
+        // ---- blocks of LU updates until enough slots have finished
+        for (;;) {
+            uint32_t e[ILP];
+            lazy_block<A, ILP, LU>(x, y, x2, y2, cr, ci, r2, e);
+            bool fin[ILP];
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) {
+                // live: n < iterMax, so the cap keeps n <= iterMax (no uint32 overflow)
+                const uint32_t inc = min(e[s] < LU ? e[s] + 1u : LU, p.iter_max - n[s]);
+#if MANDEL_LAZY_PROF
+                prof[(more ? 0 : 3) + (live[s] ? 0 : 2)] += live[s] ? inc : LU;
+                if (live[s]) prof[more ? 1 : 4] += LU - inc;
+#endif
+                if (live[s]) n[s] += inc;
+                fin[s] = live[s] && (e[s] < LU || n[s] == p.iter_max);
+            }
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) live[s] = live[s] && !fin[s];
+            if (more) {
+                bool want = false;
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) want |= !live[s];
+                if (__popc(__ballot_sync(FULL, want)) >= refill_at) break;
+            } else {  // draining: run until every slot is done
+                bool go = false;
+#pragma unroll
+                for (int s = 0; s < ILP; ++s) go |= live[s];
+                if (!__any_sync(FULL, go)) break;
+            }
+        }
+
+        // ---- retire the finished slots (a5, +a6 when dst is rank 0's peer image)
 #pragma unroll
         for (int s = 0; s < ILP; ++s) {
-            const bool done = has[s] && (lv[s] == 0 || n[s] == p.iter_max);
-            if (done) {
+            if (has[s] && !live[s]) {
                 *dst[s] = n[s];
                 my_iters += n[s];
                 my_pix += 1;
                 has[s] = false;
-                lv[s] = 0;
                 x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;  // idle: z = 0 forever
             }
-            need[s] = __ballot_sync(FULL, done);
         }
     }
+#if MANDEL_LAZY_PROF
+    for (int q = 0; q < 8; ++q) {
+        unsigned long long v = q < 6 ? prof[q] : (lane == 0 ? prof[q] : 0ull);
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) atomicAdd(&g_lazy_prof[q], v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&g_lazy_prof_done, 1u) == gridDim.x - 1) {
+            printf("LAZY_PROF live %llu past_escape %llu finished_or_idle %llu | drain live %llu past_escape %llu "
+                   "finished_or_idle %llu | runs %llu drain_runs %llu\n",
+                   g_lazy_prof[0], g_lazy_prof[1], g_lazy_prof[2], g_lazy_prof[3], g_lazy_prof[4],
+                   g_lazy_prof[5], g_lazy_prof[6], g_lazy_prof[7]);
+            for (int q = 0; q < 8; ++q) g_lazy_prof[q] = 0;
+            g_lazy_prof_done = 0;
+        }
+    }
+#endif
     flush_stats(p, my_iters, my_pix);
 }
 
@@ -1110,6 +1146,5 @@ escape_static_kernel(const Params p) {
 
 #undef MANDEL_STEP
 #undef MANDEL_STEP_SLOT
-#undef LAZY_STEP_SLOT
 
 }  // namespace mandel
