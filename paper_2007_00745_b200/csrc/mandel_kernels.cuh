@@ -524,31 +524,29 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                 }
                 k += (nb0 - nb) * BT;  // batches completed without a hit
                 if (!hit) break;
-                uint32_t ne[ILP], lv[ILP];
+                uint32_t e[ILP];  // the slot's first escaping update in the batch (BT: none)
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
                     if constexpr (A::kPacked) x[s] = sx[s];
                     else x[s] = A::half(t0[s]);  // (x + x) * 0.5 = x exactly
                     y[s] = sy[s];
                     A::resq(x[s], y[s], x2[s], y2[s]);
-                    lv[s] = rem[s] != kIdleRem ? 1u : 0u;
-                    ne[s] = 0;
+                    e[s] = BT;
                 }
 #pragma unroll
                 for (int u = 0; u < BT; ++u) {
 #pragma unroll
                     for (int s = 0; s < ILP; ++s) {
                         A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
-                        const bool in_ = !(A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2);
-                        ne[s] += lv[s];
-                        lv[s] = in_ ? lv[s] : 0u;
+                        if (A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2) e[s] = min(e[s], (uint32_t)u);
                     }
                 }
                 bool any_esc = false;
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
-                    fin[s] = rem[s] != kIdleRem && lv[s] == 0u;
-                    kx[s] = k + ne[s];
+                    // idle slots (z = c = 0) never escape; R3 counts the escaping update
+                    fin[s] = rem[s] != kIdleRem && e[s] < (uint32_t)BT;
+                    kx[s] = k + e[s] + 1u;
                     any_esc |= fin[s];
                 }
                 k += BT;
