@@ -119,6 +119,11 @@ EDGE = [
     wl.Config("ragged", -2.2, 0.8, -1.3, 1.1, 257, 33, 500, 2.0, "fp64"),
     wl.Config("it1", -2.5, 1.5, -2.0, 2.0, 64, 64, 1, 2.0, "fp64"),
     wl.Config("it2", -2.5, 1.5, -2.0, 2.0, 64, 64, 2, 2.0, "fp32"),
+    # iterMax just off the LAZY block length (16) and the batch lengths: counts capped
+    # inside a block, escapes in the same block as the cap
+    wl.Config("it17", -2.2, 0.8, -1.3, 1.3, 96, 70, 17, 2.0, "fp64"),
+    wl.Config("it33_f32", -2.2, 0.8, -1.3, 1.3, 96, 70, 33, 2.0, "fp32"),
+    wl.Config("it15_fma", -0.76, -0.73, 0.09, 0.12, 80, 60, 15, 2.0, "fp64fma"),
     wl.Config("far", -1e300, 1e300, -1e300, 1e300, 40, 40, 100, 2.0, "fp64"),
     wl.Config("R20", -2.5, 1.5, -2.0, 2.0, 120, 90, 2000, 20.0, "fp64"),
     wl.Config("Rsmall", -1.0, 0.5, -0.7, 0.7, 100, 100, 400, 0.75, "fp32"),
