@@ -749,7 +749,7 @@ escape_refill_kernel(const Params p) {
 // escape, which dominates where neighbouring counts differ (C4's zoom: one escape
 // every ~2 warp-updates).  The block form replaced a per-update `n += live; live &=
 // in` (1.5 more instructions per slot-update): C4 1739 -> 1770 Giter/s
-// (profiles/r01u_sweep_lazy_record.jsonl).
+// (profiles/r01w_sweep_lazy_record.jsonl).
 // ---------------------------------------------------------------------------
 // LU: updates between two exit tests; the exit is a refill decision only, so the
 // interval changes no count.  C4 (refill_lanes 16): LU 2 -> 1543, 4 -> 1664,
