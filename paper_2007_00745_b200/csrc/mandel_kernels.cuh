@@ -17,8 +17,9 @@
 //
 // Kernels: escape_refill_kernel (EAGER: persistent CTAs, 2-D warp tiles, lane refill;
 // the default loop tests |z|^2 every B updates and replays a hit batch exactly,
-// DESIGN.md R18 -- eager_run), escape_lazy_kernel (LAZY: per-update exact escape
-// record, refill when enough lanes are free; the default for incoherent views),
+// DESIGN.md R18 -- eager_run), escape_lazy_kernel (LAZY: exact test after every
+// update, first escape recorded per block of 16 updates, refill when enough lanes
+// hold a finished slot; chosen for incoherent views),
 // escape_adaptive_kernel (switches between the two per warp), escape_static_kernel
 // (one pixel per thread; the A/B baseline).  Arithmetic policies: ArithF64,
 // ArithF64Fma (MANDEL_FP64_FMA, R17), ArithF32, ArithF32P (packed FP32x2 loop).
