@@ -55,3 +55,39 @@ def test_device_colour_matches_oracle(mandel, oracle, mode, shape):
     big = torch.zeros(H * W * 3 + 1, dtype=torch.uint8, device="cuda:0")
     mandel.mandel_colorize(counts, big.data_ptr() + 1, W, H, cfg.iter_max, mode, None)
     assert np.array_equal(big[1:].cpu().numpy().reshape(H, W, 3), want)
+
+
+def _gray_probe_counts(M: int) -> np.ndarray:
+    """Every count for small iterMax; for large ones the ends and, for each grey level k,
+    the counts around the half-up rounding point t = (2k+1)(M-1)/510 (t = n-1)."""
+    if M <= 4096:
+        return np.arange(1, M + 1, dtype=np.uint64)
+    K = M - 1
+    ns = {1, 2, 3, M - 2, M - 1, M}
+    for k in range(256):
+        t0 = ((2 * k + 1) * K) // 510
+        for d in (-2, -1, 0, 1, 2):
+            t = t0 + d
+            if 0 <= t <= K:
+                ns.add(t + 1)
+    return np.array(sorted(ns), dtype=np.uint64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M", [2, 3, 255, 256, 257, 511, 1000, 4096, 65537, 10_000_019, 2**24 + 1,
+                               2**31 + 11, 2**32 - 2])
+def test_device_gray_rounding_points(mandel, M):
+    """The gray ramp's float estimate + exact correction against the integer formula
+    (oracle/colour.py) at every rounding point, iterMax up to 2^32 - 2."""
+    import torch
+    n = _gray_probe_counts(M)
+    pad = (-len(n)) % 4 + 4  # an aligned multiple of 4 plus a few more pixels
+    n = np.concatenate([n, np.full(pad, M, dtype=np.uint64)]).astype(np.uint32)
+    want = C.colour(n, M, C.GRAY)
+    dev = torch.from_numpy(n.view(np.int32)).to("cuda:0")
+    for W, H, off in ((len(n), 1, 0), (len(n) - 3, 1, 1)):  # vector and scalar kernel paths
+        rgb = torch.zeros(W * 3 + 1, dtype=torch.uint8, device="cuda:0")
+        mandel.mandel_colorize(dev, rgb.data_ptr() + off, W, H, M, "gray", None)
+        torch.cuda.synchronize()
+        got = rgb[off:off + W * 3].cpu().numpy().reshape(W, 3)
+        assert np.array_equal(got, want[:W]), M
