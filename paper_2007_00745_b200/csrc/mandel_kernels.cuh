@@ -438,10 +438,11 @@ __device__ __forceinline__ void flush_stats(const Params& p, unsigned long long 
     }
 }
 
-// Batched check (BT z-updates, then one |z|^2): true if any lane of the warp has a
-// slot whose final |z|^2 key reaches r2b (below key(R2); R18).
+// Batched check (BT z-updates, then one |z|^2): true if one of this thread's slots has
+// a final |z|^2 key reaching r2b (below key(R2); R18).  The warp-wide hit is
+// the vote of this predicate (batch_hit).
 template <typename A, int ILP, int BT, typename T>
-__device__ __forceinline__ bool batch_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
+__device__ __forceinline__ bool batch_key_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
                                           const T (&cr)[ILP], const T (&ci)[ILP], uint32_t r2b,
                                           uint32_t oz, const T (&t0)[ILP]) {
 #pragma unroll
@@ -467,7 +468,7 @@ __device__ __forceinline__ bool batch_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP]
     uint32_t m = 0;
 #pragma unroll
     for (int s = 0; s < ILP; ++s) m = max(m, A::ukey(A::sumsq(x[s], y[s], x2[s], y2[s])));
-    return __any_sync(0xffffffffu, m >= r2b);
+    return m >= r2b;
 }
 
 // ---------------------------------------------------------------------------
@@ -519,11 +520,16 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                         else t0[s] = A::add(x[s], x[s]);
                         sy[s] = y[s];
                     }
-                    hit = batch_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero, t0);
-                    if (hit) break;
-                    if (--nb == 0) break;
+                    // one vote and one branch leave the loop on a hit or at the budget
+                    const bool h = batch_key_hit<A, ILP, BT>(x, y, x2, y2, cr, ci, r2b, p.opaque_zero, t0);
+                    --nb;
+                    if (__any_sync(FULL, h || nb == 0)) {
+                        hit = __any_sync(FULL, h);
+                        break;
+                    }
                 }
-                k += (nb0 - nb) * BT;  // batches completed without a hit
+                k += (nb0 - nb) * BT;  // batches run, the hit batch included ...
+                if (hit) k -= BT;      // ... which is counted after its replay
                 if (!hit) break;
                 uint32_t e[ILP];  // the slot's first escaping update in the batch (BT: none)
 #pragma unroll
