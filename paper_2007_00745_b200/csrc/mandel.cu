@@ -295,7 +295,7 @@ struct KernelChoice {
     int bt;          // EAGER: z-updates per escape check (1 = every update; 4, 8, 16 = batched, R18)
     int packed = 0;  // fp32 batched loop on FADD2/FMUL2 slot pairs (set by build_params)
 };
-// ILP2 runs with ptxas' unconstrained schedule (72 registers, 3 CTAs of 256 threads per SM).
+// ILP2 runs with ptxas' unconstrained schedule (74 registers, 3 CTAs of 256 threads per SM).
 // Batched escape check with a whole-batch replay on a hit (R18), measured per config
 // (profiles/r01_sweep_batch.jsonl, Giter/s): fp64 C2 check-every-8 ILP2 2061 (per-update
 // check 1722), C5 2360 (1962); fp32 C3 check-every-8 ILP1 3346 (per-update ILP4 2504).
