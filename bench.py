@@ -527,6 +527,7 @@ def cpu_baseline(cfg, cpu_seconds, gpu_img=None):
            "sample": f"{len(rows)} evenly strided rows of {cfg.name} ({len(rows)}/{cfg.H} rows, "
                      f"{iters} pixel-iterations), plain C oracle (-O2 -ffp-contract=off) on "
                      f"{used} host threads claiming {chunk}-row chunks", "seconds": round(dt, 3),
+           "core_seconds": round(dt * used, 2),  # the sample's CPU work (target --cpu-seconds)
            "per_core": round(iters / dt / 1e9 / used, 5)}
     # single-threaded rate: every 8th row of the same sample, one thread
     srows = rows[::8]
