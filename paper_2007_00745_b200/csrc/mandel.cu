@@ -1344,8 +1344,10 @@ int mandel_colorize(const uint32_t* counts_dev, uint8_t* rgb_dev, uint32_t W, ui
     const uint64_t npix = (uint64_t)W * H;
     const bool aligned = ((uintptr_t)counts_dev % 16 == 0) && ((uintptr_t)rgb_dev % 4 == 0);
     const unsigned grid = (unsigned)(sms * 8);  // 8 x 256-thread CTAs per SM, grid-stride
-    if (aligned) mandel::colourize_kernel<<<grid, 256, 0, s>>>(counts_dev, rgb_dev, npix, iterMax, mode);
-    else mandel::colourize_scalar_kernel<<<grid, 256, 0, s>>>(counts_dev, rgb_dev, npix, iterMax, mode);
+    const float scale = iterMax > 1 ? (float)(255.0 / (double)(iterMax - 1)) : 0.0f;  // any estimate works:
+    // the kernel corrects it exactly (mandel_image.cuh, colour_rgb)
+    if (aligned) mandel::colourize_kernel<<<grid, 256, 0, s>>>(counts_dev, rgb_dev, npix, iterMax, mode, scale);
+    else mandel::colourize_scalar_kernel<<<grid, 256, 0, s>>>(counts_dev, rgb_dev, npix, iterMax, mode, scale);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     return MANDEL_OK;

@@ -65,9 +65,10 @@ __device__ __forceinline__ uint32_t colour_rgb(uint32_t n, uint32_t iter_max, in
     return n < iter_max ? px : 0u;  // bytes r, g, b (little-endian); interior black
 }
 
+// scale = 255/(iterMax-1) as a float, computed on the host (a device float division
+// would bring FFMA-based code into the library, which the SASS gate forbids)
 __global__ void colourize_kernel(const uint32_t* __restrict__ counts, uint8_t* __restrict__ rgb,
-                                 uint64_t npix, uint32_t iter_max, int mode) {
-    const float scale = iter_max > 1 ? 255.0f / (float)(iter_max - 1) : 0.0f;
+                                 uint64_t npix, uint32_t iter_max, int mode, float scale) {
     const bool small = iter_max <= (1u << 22);
     const uint64_t ngroups = npix / 4;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -95,8 +96,7 @@ __global__ void colourize_kernel(const uint32_t* __restrict__ counts, uint8_t* _
 
 // unaligned fallback: one pixel per thread per step
 __global__ void colourize_scalar_kernel(const uint32_t* __restrict__ counts, uint8_t* __restrict__ rgb,
-                                        uint64_t npix, uint32_t iter_max, int mode) {
-    const float scale = iter_max > 1 ? 255.0f / (float)(iter_max - 1) : 0.0f;
+                                        uint64_t npix, uint32_t iter_max, int mode, float scale) {
     const bool small = iter_max <= (1u << 22);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npix; i += stride) {
