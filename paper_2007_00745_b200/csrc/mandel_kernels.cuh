@@ -487,10 +487,10 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
     const int r2c = p.r2cand;
     const uint32_t r2b = p.r2batch;
     bool esc[ILP];
-    // ---- iterate: Eq. 1 on every slot until some slot is finished.  The hot loop
-    // tests a 32-bit candidate key (one compare per slot); on a candidate the warp
-    // leaves the loop and verifies the exact 64-bit test, resuming on a false alarm.
-    // BT > 1 (batched check, R18): BT z-updates per test and |z|^2 only
+    // ---- iterate: Eq. 1 on every slot until some slot is finished.  BT = 1: the loop
+    // tests a 32-bit candidate key (one compare per slot) after every update; on a
+    // candidate the warp leaves the loop and verifies the exact 64-bit test, resuming
+    // on a false alarm.  BT > 1 (batched check, R18): BT z-updates per test and |z|^2 only
     // after the last one, against a threshold below R2 that every slot which escaped
     // inside the batch still exceeds (|z| grows after an escape when R >= 2); on a
     // hit the warp restores the batch-start state and replays the batch with the
@@ -500,11 +500,11 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
     bool lazy_exit = false;
     for (;;) {
         if (BT > 1) {
-            // only z = (x, y) is saved at the batch start; on a hit A::resq rebuilds
-            // the carried squares from it with the same operations (identical bits),
-            // and the whole batch is replayed with the exact per-update test, each
-            // slot's escaping update recorded in-loop; every slot that escaped in the
-            // batch is then retired at once
+            // only z is kept at the batch start (x as x + x, which the first update
+            // consumes anyway; y copied); on a hit A::resq rebuilds the carried squares
+            // from it with the same operations (identical bits), and the whole batch is
+            // replayed with the exact per-update test, each slot's first escaping update
+            // recorded; every slot that escaped in the batch is then retired at once
             while (kmax - k >= BT) {
                 T sx[ILP], sy[ILP];
                 bool hit;
