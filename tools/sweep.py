@@ -33,7 +33,7 @@ def main():
     ap.add_argument("--tile-rows", default="0", help="rows per tile, comma separated (0 = default)")
     ap.add_argument("--pack", default="1", help="fp32 packed batched loop: 1, 0 or 1,0")
     ap.add_argument("--chunks", default="16")
-    ap.add_argument("--lanes", default="8")
+    ap.add_argument("--lanes", default="0", help="LAZY refill_lanes (0 = the library default, 16)")
     ap.add_argument("--minb", default="1")
     ap.add_argument("--adapt", default="16:64", help="lo:hi pairs, comma separated")
     ap.add_argument("--steps", type=int, default=10)
