@@ -661,6 +661,11 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
                                   {MANDEL_KERNEL_LAZY, 2, 1, 1}};
     mandel_options po{};
     if (o) po = *o;
+    // the probe characterises the view, not the launch: it always runs on the whole
+    // GPU, the geometry its threshold was calibrated in (on an SM slice, options.max_sms,
+    // the sample has no drain phase and reads fewer iterations per exit -- the paper
+    // grid on 4 SMs picked LAZY, 16% slower than EAGER there)
+    po.max_sms = 0;
     // one eager launch over the sample: its iterations per loop exit measure how
     // incoherent the escapes are (C2 ~29, C5 ~68, C4's zoom ~3 at ILP2)
     cudaEvent_t e0, e1;
