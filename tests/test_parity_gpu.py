@@ -522,3 +522,21 @@ def test_async_host_rejects_misuse(mandel):
         mandel.mandel_render_ex(*v.args(), "fp64", "fcfs", 2, out_host=o, async_host=True, want_stats=False,
                                 logical_ranks=True)
     mandel.mandel_finish()
+
+
+@pytest.mark.gpu
+def test_view_probe_ignores_sm_slicing(mandel, oracle):
+    """The EAGER/LAZY view probe characterises the view, not the launch: with
+    options.max_sms it still runs on the whole GPU (its calibration geometry), so a
+    sliced first render makes the same choice from the same statistic as a whole-GPU
+    one (on a 4-SM slice the sample had no drain phase and read fewer iterations per
+    exit: the paper grid picked LAZY, 16% slower there)."""
+    cfg = wl.Config("probe", -2.5, 1.5, -2.0, 2.0, 2048, 2048, 2000, 20.0, "fp64")
+    got = []
+    for kw in ({"max_sms": 4}, {}):
+        mandel.mandel_shutdown()  # clears the per-view choice cache
+        out, st = _render_dev(mandel, cfg, "block", 1, **kw)
+        got.append((st["kernel"], st["probe"][1]))
+    (k0, ipe0), (k1, ipe1) = got
+    assert k0 == k1, got
+    assert abs(ipe0 - ipe1) <= 0.1 * ipe1, got
