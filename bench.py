@@ -58,7 +58,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2", choices=sorted(wl.CONFIGS))
-    ap.add_argument("--scheme", default="fcfs", choices=["block", "cyclic", "fcfs"])
+    ap.add_argument("--scheme", default=None, choices=["block", "cyclic", "fcfs"],
+                    help="row partition (PAPER.md §III); default: fcfs over N > 1 GPUs, and on one GPU "
+                         "the plain row order (block: one rank owns every row -- there is nothing to "
+                         "partition; FCFS on one rank would only add its claim lookups, per_scheme "
+                         "times all three)")
     ap.add_argument("--chunk-rows", type=int, default=16)
     ap.add_argument("--kernel", default="refill",
                     help="refill (default), static, eager, lazy, adaptive, refill1..4, lazy1/2")
@@ -164,6 +168,8 @@ def aggregate(dist, rank_ms: float, rank_iters: int, device=None):
 # ---------------------------------------------------------------------------
 def run_ours(args):
     import torch
+    if args.scheme is None:
+        args.scheme = "block" if dist_env()[0] == 1 else "fcfs"
 
     from paper_2007_00745_b200 import mandel
 
@@ -211,6 +217,7 @@ def run_ours(args):
     shared = None  # N > 1 e2e: the shared host image every rank drains a slice into
 
     def step(scheme, out_host=None, e2e=False, sync=True):
+        """One render (N > 1: this rank's rows; the caller adds the device barrier)."""
         if world == 1:
             if e2e:
                 # host output through the library, asynchronous and pipelined: render n+1
@@ -235,10 +242,18 @@ def run_ours(args):
             _d2h(out_host, img_ptr, nbytes, s_handle)  # rank 0 holds the whole map
         return st
 
-    def timed(scheme, steps, warmup, sampler=None, out_host=None, e2e=False):
+    def timed(scheme, steps, warmup, sampler=None, out_host=None, e2e=False, barriered=True):
+        """K renders bracketed by barrier + synchronize, max over ranks (the caller reduces).
+        N > 1 and barriered: a device-side barrier (rr.device_barrier: an all_reduce on the
+        render stream) follows every render, so render n+1 starts on every rank only after
+        every rank finished render n -- each step is one whole render to the moment rank 0
+        holds the map, FCFS tail included.  barriered=False: renders follow
+        each other without a barrier (render n+1 fills render n's tail; pipelined)."""
         stats = []
         for _ in range(warmup):
             step(scheme, out_host, e2e)
+            if world > 1 and barriered and not e2e:
+                rr.device_barrier()
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -258,6 +273,8 @@ def run_ours(args):
             st = step(scheme, out_host, e2e, sync=(i == steps - 1))
             if ev:
                 ev[i][1].record(stream)
+            if world > 1 and barriered and not e2e:
+                rr.device_barrier()
             if st is not None:
                 stats.append(st)
         if e2e and world == 1:
@@ -311,6 +328,8 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         return e0.elapsed_time(e1)
 
+    # the FP pipe peak of this GPU, measured live before the timed region (tools/fp_peak)
+    peak_meas = measured_fp_peak(cfg.dtype) if rank == 0 else None
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -328,32 +347,45 @@ def run_ours(args):
     kern_ms = stats[-1]["render_ms_mean"]  # mean per-render duration over the timed region
     kern_ms_all, _ = aggregate(dist, kern_ms, 0, adev)
     clocks = sampler.summary()
+    if clocks is not None:
+        # the SM clock the escape kernels themselves measured (clock64 / %globaltimer per
+        # CTA, mandel_stats.sm_clock_mhz) on the last timed render, next to nvidia-smi's
+        clocks["sm_mhz_in_kernel"] = round(stats[-1].get("sm_clock_mhz", 0.0), 1)
 
     # roofline of the dominant kernel (the escape kernel): algorithmic FP ops per launch
     # (8 per pixel-iteration of this rank) / its CUDA-event duration on the launching stream
     achieved = iters_launch * FLOPS_PER_ITER / (kern_ms * 1e-3) / 1e12
-    peak = fp_peak_tflops(cfg.dtype)
+    peak_uc = fp_peak_tflops(cfg.dtype)
+    peak, peak_src = (peak_meas["tflops"], peak_meas["source"]) if peak_meas else (peak_uc, "unit counts")
+    lanes = FP64_LANES if cfg.dtype == "fp64" else FP32_LANES
     roof = {"bound": "alu", "unit": "TFLOP/s", "achieved": round(achieved, 4),
             "peak": round(peak, 4), "frac": round(achieved / peak, 4),
             "traffic": None,
-            "peak_basis": f"{SMS} SMs x {FP64_LANES if cfg.dtype == 'fp64' else FP32_LANES} "
-                          f"{cfg.dtype.upper()} lanes x {SM_MAX_MHZ:.0f} MHz (guide unit counts, "
-                          "max clock; DESIGN.md Roofline)",
+            "peak_basis": f"measured: {peak_src}",
+            # the guide's unit-count figure beside the measured one
+            "peak_unit_count": round(peak_uc, 4), "frac_unit_count": round(achieved / peak_uc, 4),
+            "peak_unit_count_basis": f"{SMS} SMs x {lanes} {cfg.dtype.upper()} lanes x {SM_MAX_MHZ:.0f} MHz "
+                                     "(max SM clock; DESIGN.md Roofline)",
             "kernel_ms": round(kern_ms, 4),
-            "ops_per_launch": int(iters_launch * FLOPS_PER_ITER)}
+            "ops_per_launch": int(iters_launch * FLOPS_PER_ITER),
+            "ops_per_launch_basis": f"{FLOPS_PER_ITER} FP ops (3 mul + 5 add/sub) x {iters_launch:.0f} "
+                                    "pixel-iterations (sum of this rank's counts) per launch"}
     prof = _traffic_from_profiles(cfg, world)
     if prof:
-        # from the committed ncu --set full capture of this kernel (profiles/): DRAM bytes
-        # per launch, and the FP pipe utilisation the kernel actually EXECUTED -- the
-        # batched escape check (R18) executes fewer than 8 FP ops per counted iteration,
-        # so `frac` (counted ops) can exceed the executed pipe utilisation
+        # NOT measured in this run: read from the committed ncu --set full capture of this
+        # kernel (profiles/): DRAM bytes per launch, and the FP pipe utilisation the kernel
+        # actually EXECUTED -- the batched escape check (R18) executes fewer than 8 FP ops
+        # per counted iteration, so `frac` (counted ops) can exceed the executed utilisation
         roof["traffic"] = prof.get("dram_bytes_per_launch")
         pipe = prof.get("fp64_pipe_active_pct" if cfg.dtype != "fp32" else "fma_pipe_active_pct")
         if pipe is not None:
             roof["ncu_pipe_active"] = round(pipe / 100.0, 4)
         roof["ncu_kernel"] = prof.get("kernel")
+        roof["traffic_source"] = (f"profiles/{os.path.basename(prof['_path'])}: committed ncu --set full "
+                                  "capture of this kernel on this config (not measured in this run)")
     if clocks and clocks.get("sm_mhz"):
-        roof["frac_at_measured_clock"] = round(achieved / fp_peak_tflops(cfg.dtype, clocks["sm_mhz"]), 4)
+        roof["frac_unit_count_at_measured_clock"] = round(
+            achieved / fp_peak_tflops(cfg.dtype, clocks["sm_mhz"]), 4)
 
     line = {
         "metric": "pixel-iterations/sec (Giter/s)",
@@ -378,6 +410,11 @@ def run_ours(args):
                         f"iterMax {cfg.iter_max}, R {cfg.R}, {cfg.dtype}",
             "scheme": args.scheme, "chunk_rows": args.chunk_rows, "kernel": args.kernel,
             "sum_iters_per_step": iters_job, "pixels": cfg.pixels,
+            # what the kernels ran: the row order, and the FCFS claims the device counted
+            # (Eq. 19 analog; ceil(H/chunk) per render when complete), summed over ranks
+            "kernel_scheme": stats[-1].get("kernel_scheme"),
+            "chunks_claimed_per_step": sum_over_ranks(dist, [stats[-1]["chunks_claimed"]], adev)[0],
+            "kernel_variant": stats[-1].get("kernel"),
             "parallelism": f"{args.scheme} rows over {world} GPU(s)",
             "gather": "none (1 GPU)" if world == 1 else (
                 "fused: every rank's kernel stores into rank 0's map over NVLink (CUDA IPC)"
@@ -390,6 +427,23 @@ def run_ours(args):
         "roofline": roof,
         "clocks": clocks,
     }
+
+    if world > 1:
+        # the headline steps above are barriered (each render whole before the next);
+        # efficiency is judged on them.  Pipelined throughput beside it: the same renders
+        # with no barrier between them (render n+1 fills render n's tail)
+        line["render_ms_barriered"] = line["ms_per_step"]
+        pms, _ = timed(args.scheme, args.steps, 2, barriered=False)
+        pms_job, _ = aggregate(dist, pms, 0, adev)
+        line["pipelined"] = {"value": round(iters_job / (pms_job / args.steps * 1e-3) / 1e9, 3),
+                             "ms_per_step": round(pms_job / args.steps, 4),
+                             "note": "renders back to back with no barrier between them: a fast rank's "
+                                     "render n+1 overlaps render n's tail -- not the paper's per-render "
+                                     "time; scaling efficiency is judged on `value` (barriered)"}
+        line["timing"] = ("each timed step is one render followed by a device-side barrier (a 1-element "
+                          "NCCL all_reduce on the render stream): render n+1 starts on every rank after "
+                          "every rank finished render n; K steps bracketed by barrier + synchronize, "
+                          "max over ranks")
 
     if not args.profile:
         # e2e: the same metric through the C ABI with a HOST destination (pinned), the
@@ -425,6 +479,31 @@ def run_ours(args):
             total = shared.checksum() if (world > 1 and shared.ok) else \
                 int(host.numpy().view(np.uint32).sum(dtype=np.uint64))
             line["e2e"]["map_sum_check"] = total == (iters_rank if world == 1 else iters_job)
+        # latency: ONE synchronous render with the whole map landing in host memory --
+        # the paper's "total process time", no overlap between
+        # renders; the median of a few calls, host wall clock around the call (max over ranks)
+        lat = []
+        for _ in range(5):
+            if dist is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            if world == 1:
+                mandel.mandel_render_ex(*cfg.args(), cfg.dtype, args.scheme, 1, out_host=host,
+                                        stream0=s_handle, chunk_rows=args.chunk_rows, kernel=kernel)
+            else:
+                rr.step(args.scheme, barrier=True, sync=True, chunk_rows=args.chunk_rows, kernel=kernel)
+                if shared.ok:
+                    shared.drain(img_ptr, cfg.W, cfg.H, world, s_handle)
+                    dist.barrier()
+                elif rank == 0:
+                    _d2h(host, img_ptr, nbytes, s_handle)
+            lat_ms = (time.perf_counter() - t0) * 1e3
+            lat_ms, _ = aggregate(dist, lat_ms, 0, adev)
+            lat.append(lat_ms)
+        line["e2e"]["latency_ms"] = round(statistics.median(lat), 4)
+        line["e2e"]["latency_note"] = ("one synchronous render + the whole map in pinned host memory, "
+                                       "host wall clock around the call, median of 5 (the paper's total "
+                                       "process time); `value` above overlaps consecutive renders")
         if shared is not None:
             shared.close()
             shared = None
@@ -438,7 +517,14 @@ def run_ours(args):
                 sms, sst = timed(sch, k, 2)
                 sms_job, _ = aggregate(dist, sms, 0, adev)
                 per[sch] = {"value": round(iters_job / (sms_job / k * 1e-3) / 1e9, 3),
-                            "ms_per_step": round(sms_job / k, 4), "steps": k}
+                            "ms_per_step": round(sms_job / k, 4), "steps": k,
+                            "kernel_scheme": sst[-1].get("kernel_scheme"),
+                            "chunks_claimed": sst[-1].get("chunks_claimed")}
+                if world > 1:
+                    per[sch]["render_ms_barriered"] = per[sch]["ms_per_step"]
+                    pms, _ = timed(sch, k, 2, barriered=False)
+                    pms_job, _ = aggregate(dist, pms, 0, adev)
+                    per[sch]["pipelined_value"] = round(iters_job / (pms_job / k * 1e-3) / 1e9, 3)
             line["per_scheme"] = per
 
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -498,7 +584,38 @@ def _traffic_from_profiles(cfg, world):
             continue
         if d.get("config") == cfg.name and d.get("n_gpus", 1) == world:
             best = d
+            best["_path"] = p
     return best
+
+
+def measured_fp_peak(dtype: str):
+    """The FP pipe peak measured on this GPU right now: tools/fp_peak (8 independent
+    DADD/DMUL -- FADD/FMUL for fp32 -- chains per thread at full occupancy; no FMA, as in
+    the path), mean of the add and mul figures, in T lane-ops/s.  Falls back to the newest
+    committed profiles/*fp_peak.json when the tool is not built or fails."""
+    import glob
+    exe = os.path.join(ROOT, "tools", "fp_peak")
+    keys = ("dadd", "dmul") if dtype != "fp32" else ("fadd", "fmul")
+    if os.access(exe, os.X_OK):
+        try:
+            r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+            d = json.loads(r.stdout)
+            return {"tflops": sum(d[k]["tops"] for k in keys) / 2,
+                    "source": f"tools/fp_peak run live before the timed region ({keys[0]}/{keys[1]} chains, "
+                              f"{d['sms']} SMs x {d['ctas_per_sm']} CTAs; implied clock "
+                              f"{d[keys[0]].get('implied_mhz', 0):.0f} MHz)"}
+        except (OSError, ValueError, KeyError, subprocess.SubprocessError):
+            pass
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_fp_peak.json")))
+    for p in reversed(files):
+        try:
+            d = json.load(open(p))
+            return {"tflops": sum(d[k]["tops"] for k in keys) / 2,
+                    "source": f"profiles/{os.path.basename(p)} (committed tools/fp_peak run on a B200; "
+                              "the tool was not runnable here)"}
+        except (OSError, ValueError, KeyError):
+            continue
+    return None
 
 
 # ---------------------------------------------------------------------------

@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 6
+#define MANDEL_ABI_VERSION 7
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -110,7 +110,9 @@ typedef struct mandel_stats {
     uint64_t rank_iters[MANDEL_MAX_GPUS];  /* per-rank pixel-iterations                            */
     uint64_t rank_pixels[MANDEL_MAX_GPUS]; /* per-rank pixels                                      */
     uint32_t rank_rows[MANDEL_MAX_GPUS];   /* per-rank rows started (FCFS: claimed chunk rows)     */
-    uint32_t chunks_claimed;       /* FCFS successful global claims (= ceil(H/chunk_rows)); Eq. 19  */
+    uint32_t chunks_claimed;       /* FCFS successful global claims counted on the device by the
+                                      claiming kernels (= ceil(H/chunk_rows) when complete; Eq. 19).
+                                      0 when the kernels ran a static row order (kernel_scheme)   */
     uint32_t transfers;            /* results sent to rank 0: static schemes one band per rank != 0
                                       (N-1, Eq. 18/20); FCFS schemes the rows computed by ranks != 0
                                       (FCFS_MASTER: every row; Eq. 19 counts claim + reply = 2 H)   */
@@ -125,6 +127,13 @@ typedef struct mandel_stats {
     uint64_t loop_exits;           /* kernel-choice probe only (else 0): loop exits over warps      */
     int32_t  kernel_batch;         /* EAGER: z-updates per escape check actually run (1, 4, 8, 16)  */
     int32_t  kernel_packed;        /* 1: the fp32 batched loop ran on FADD2/FMUL2 slot pairs        */
+    double   sm_clock_mhz;         /* SM clock during the escape kernels, measured in them: the sum
+                                      over CTAs of SM cycles (clock64) / the sum of wall ns
+                                      (%globaltimer), x 1e3; over every rank and band of the call  */
+    int32_t  kernel_scheme;        /* the row order the kernels actually ran (enum mandel_scheme):
+                                      the requested scheme, except MANDEL_BLOCK for the row bands of
+                                      the pipelined one-GPU host hand-off (each band a row range)  */
+    int32_t  reserved0;
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */

@@ -152,17 +152,26 @@ int make_plan(int scheme, uint32_t H, int n, int r, Plan& pl) {
 // ---------------------------------------------------------------------------
 // Per-device and per-rank resources (cached across calls; freed by mandel_shutdown).
 // ---------------------------------------------------------------------------
+typedef void (*KernelFn)(mandel::Params);
+
 struct DeviceCtx {
     bool init = false;
     int sms = 0;
-    int occ_cache[3][5][5][6] = {};  // CTAs/SM: [fp32][variant][ilp][minb index], 0 = not queried
+    std::map<KernelFn, int> occ_cache;  // CTAs/SM per instantiated kernel (variant, ilp, budget,
+                                        // batch length and packing all change the registers)
     bool peer_to0 = false;
+    uint32_t* scratch = nullptr;  // the view probe's compact sample band (every 16th row)
+    size_t scratch_bytes = 0;
 };
 
 struct RankCtx {
     int device = -1;
     cudaStream_t stream = nullptr;
     cudaEvent_t k0 = nullptr, k1 = nullptr;
+    // recorded after every launch that reads or writes `state`; the next call's reset of
+    // the state waits on it, so enqueue-only renders on different streams never share it
+    // mid-flight (the caller may pass a different stream per call)
+    cudaEvent_t used = nullptr;
     void* state = nullptr;  // WorkState + chunk_map
     size_t state_bytes = 0;
 };
@@ -204,7 +213,6 @@ struct BusyGuard {
     ~BusyGuard() { if (ok) g_busy.store(false); }
 };
 
-typedef void (*KernelFn)(mandel::Params);
 constexpr int kVariantProbe = 99;  // internal: eager + loop statistics (kernel-choice probe)
 
 // Register-budget instantiations (min CTAs per SM in __launch_bounds__).
@@ -352,6 +360,7 @@ int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
             if (rc.stream) cudaStreamDestroy(rc.stream);
             if (rc.k0) cudaEventDestroy(rc.k0);
             if (rc.k1) cudaEventDestroy(rc.k1);
+            if (rc.used) cudaEventDestroy(rc.used);
             if (rc.state) cudaFree(rc.state);
             rc = RankCtx();
         }
@@ -363,7 +372,10 @@ int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
     if (!rc.stream) CK(cudaStreamCreateWithFlags(&rc.stream, cudaStreamDefault));
     if (!rc.k0) CK(cudaEventCreate(&rc.k0));
     if (!rc.k1) CK(cudaEventCreate(&rc.k1));
+    if (!rc.used) CK(cudaEventCreateWithFlags(&rc.used, cudaEventDisableTiming));
     if (rc.state_bytes < state_bytes) {
+        // an enqueued render may still use the old buffer
+        if (rc.state) CK(cudaEventSynchronize(rc.used));
         if (rc.state) CK(cudaFree(rc.state));
         rc.state = nullptr;
         rc.state_bytes = 0;
@@ -386,16 +398,8 @@ struct LaunchSpec {
     size_t smem = 0;  // dynamic shared memory (only to pin one CTA per SM, options.max_sms)
 };
 
-int occupancy(int device, int fp32, int variant, int ilp, int mi, KernelFn fn, int& occ) {
-    const int vi = variant == kVariantProbe ? MANDEL_KERNEL_EAGER : variant;  // same launch shape
-    int& c = g_dev[device].occ_cache[fp32][vi][variant == MANDEL_KERNEL_STATIC ? 0 : ilp][mi < 0 ? 0 : mi];
-    if (variant == kVariantProbe) {
-        CK(cudaSetDevice(device));
-        int cp = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cp, fn, mandel::kCtaThreads, 0));
-        occ = cp > 0 ? cp : 1;
-        return MANDEL_OK;
-    }
+int occupancy(int device, KernelFn fn, int& occ) {
+    int& c = g_dev[device].occ_cache[fn];
     if (c == 0) {
         CK(cudaSetDevice(device));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, fn, mandel::kCtaThreads, 0));
@@ -416,12 +420,11 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
                  size_t state_cap, uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls,
                  const Plan* band = nullptr, const KernelChoice* force = nullptr) {
-    // FCFS with a single claimant: the counter hands that rank chunks 0, 1, 2, ... in
-    // order, so the dispatch is exactly the one-rank row order; run it as such (no
-    // claim atomics or chunk-map lookups; the claim count is reported as ceil(H/chunk)).
+    // FCFS runs its claims even with a single claimant (the counter then hands out chunks
+    // 0, 1, 2, ... in order; chunks_claimed is the device's own count, Eq. 19).
     // FCFS_MASTER: rank 0 computes nothing (an empty plan, its kernel exits at once);
     // the workers run the FCFS claim path with single-row chunks by default.
-    int kscheme = (scheme == MANDEL_FCFS && nranks == 1) ? MANDEL_BLOCK : scheme;
+    int kscheme = scheme;
     Plan pl;
     int rc = make_plan(kscheme, H, nranks, rank, pl);
     if (rc) return rc;
@@ -505,6 +508,12 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     KernelChoice kc = kDefaultChoice[fi];
     if (force) {
         kc = *force;
+        // the per-view choice fixes the kernel; an explicit ilp / min_ctas still applies
+        // (mandel_render_ex and mandel_render_rank honour them alike)
+        if (kernel == MANDEL_KERNEL_REFILL && kc.variant != kVariantProbe && o) {
+            if (o->ilp) kc.ilp = o->ilp;
+            if (o->min_ctas) kc.minb = o->min_ctas;
+        }
     } else if (kernel != MANDEL_KERNEL_REFILL) {
         kc.variant = kernel;
         kc.ilp = (o && o->ilp) ? o->ilp : 2;
@@ -550,7 +559,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     ls.block = persistent ? dim3(mandel::kCtaThreads) : dim3(32, mandel::kWarpsPerCta);
     if (persistent) {
         int occ = 1;
-        int rc2 = occupancy(device, fi, kc.variant, kc.ilp, mi, ls.fn, occ);
+        int rc2 = occupancy(device, ls.fn, occ);
         if (rc2) return rc2;
         // options.max_sms: the rank is a slice of exactly that many SMs (the paper's task
         // on one core, tools/paper_tables.py): one CTA per SM -- a dynamic shared memory
@@ -570,9 +579,14 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     return MANDEL_OK;
 }
 
-uint32_t single_rank_claims(uint32_t H, const mandel_options* o) {
-    const uint32_t chunk = effective_chunk(MANDEL_FCFS, o);
-    return (uint32_t)(((uint64_t)H + chunk - 1) / chunk);
+// SM clock over a set of kernel states (mandel_stats.sm_clock_mhz): sum of cycles / sum of ns
+double clock_mhz(const mandel::WorkState* ws, int n) {
+    double cyc = 0, ns = 0;
+    for (int i = 0; i < n; ++i) {
+        cyc += (double)ws[i].clk_cycles;
+        ns += (double)ws[i].clk_ns;
+    }
+    return ns > 0 ? cyc / ns * 1e3 : 0.0;
 }
 
 size_t state_bytes_for(int scheme, uint32_t H, const mandel_options* o) {
@@ -642,8 +656,11 @@ float g_probe[2] = {0, 0};  // last probe: eager sample time (ms), eager iterati
 constexpr float kLazyBelowItersPerExit = 23.0f;
 constexpr uint32_t kProbeStride = 16;
 
+// The probe renders its sample rows into a compact band in library-owned scratch memory
+// on the probing device (band mode: band row = sample index), never into the caller's
+// map -- under mandel_render_rank that map is rank 0's shared image on another GPU.
 int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, uint32_t iter_max,
-                int dtype, const mandel_options* o, uint32_t* image, void* state, size_t state_cap,
+                int dtype, const mandel_options* o, void* state, size_t state_cap,
                 int device, cudaStream_t s, KernelChoice& out) {
     const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
     out = kDefaultChoice[fi];
@@ -657,6 +674,19 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
     }
     const uint32_t n = (H + kProbeStride - 1) / kProbeStride;
     const Plan pl{n, 0, kProbeStride, n, 0};
+    DeviceCtx& dc = g_dev[device];
+    const size_t sbytes = (size_t)n * W * sizeof(uint32_t);
+    CK(cudaSetDevice(device));
+    if (dc.scratch_bytes < sbytes) {
+        if (dc.scratch) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaFree(dc.scratch));
+        }
+        dc.scratch = nullptr;
+        dc.scratch_bytes = 0;
+        CK(cudaMalloc(&dc.scratch, sbytes));
+        dc.scratch_bytes = sbytes;
+    }
     const KernelChoice cand[2] = {{kVariantProbe, kDefaultChoice[fi].ilp, kDefaultChoice[fi].minb, 1},
                                   {MANDEL_KERNEL_LAZY, 2, 1, 1}};
     mandel_options po{};
@@ -666,6 +696,7 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
     // the sample has no drain phase and reads fewer iterations per exit -- the paper
     // grid on 4 SMs picked LAZY, 16% slower than EAGER there)
     po.max_sms = 0;
+    po.band_out = 1;  // sample row k -> scratch row k
     // one eager launch over the sample: its iterations per loop exit measure how
     // incoherent the escapes are (C2 ~29, C5 ~68, C4's zoom ~3 at ILP2)
     cudaEvent_t e0, e1;
@@ -673,14 +704,16 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     LaunchSpec ls;
-    int rc = build_params(d, W, H, iter_max, dtype, MANDEL_BLOCK, 1, 0, &po, image, state, state_cap,
+    int rc = build_params(d, W, H, iter_max, dtype, MANDEL_BLOCK, 1, 0, &po, dc.scratch, state, state_cap,
                           nullptr, false, device, ls, &pl, &cand[0]);
     if (rc) { cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
+    CK(cudaStreamWaitEvent(s, g_rank[0].used, 0));  // an enqueued render may still use the state
     CK(cudaMemsetAsync(state, 0, state_cap, s));
     CK(cudaEventRecord(e0, s));
     rc = launch(ls, s);
     if (rc) { cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
     CK(cudaEventRecord(e1, s));
+    CK(cudaEventRecord(g_rank[0].used, s));
     mandel::WorkState ws;
     CK(cudaMemcpyAsync(&ws, state, sizeof(ws), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -856,7 +889,9 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         stats->d2h_ms = ms - kend;  // the part of the hand-off not hidden behind compute
         stats->rank_iters[0] = stats->sum_iters;
         stats->rank_pixels[0] = stats->pixels;
-        stats->chunks_claimed = is_dynamic(scheme) ? single_rank_claims(H, opts) : 0u;
+        stats->chunks_claimed = 0;  // the bands are row ranges: no claims
+        stats->kernel_scheme = MANDEL_BLOCK;
+        stats->sm_clock_mhz = clock_mhz(ws.data(), bands);
         stats->transfers = 0;
         stats->kernel_launches = (uint32_t)bands;
         stats->ngpus = 1;
@@ -927,7 +962,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         rc = ensure_rank(0, 0, sbytes, nullptr);
         if (rc) return rc;
         cudaStream_t sp = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
-        rc = auto_choice(d, bounds, W, H, iter_max, dtype, opts, image, g_rank[0].state,
+        rc = auto_choice(d, bounds, W, H, iter_max, dtype, opts, g_rank[0].state,
                          g_rank[0].state_bytes, 0, sp, kc);
         if (rc) return rc;
     }
@@ -977,6 +1012,9 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
     // rank 0 orders everything: reset state, start event, then every rank waits on it
     CK(cudaSetDevice(0));
+    // the counter and the rank states are library-owned and reused: an earlier enqueued
+    // render (possibly on another stream) must be done with them before they are reset
+    for (int r = 0; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].used, 0));
     CK(cudaMemsetAsync(g_root.fcfs_ctr, 0, 256, s0));
     CK(cudaMemsetAsync(g_rank[0].state, 0, sbytes, s0));
     CK(cudaEventRecord(g_root.start, s0));
@@ -1000,6 +1038,12 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     CK(cudaSetDevice(0));
     for (int r = 1; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].k1, 0));
     CK(cudaEventRecord(g_root.done, s0));
+    // every rank's state and the shared counter are free once GPU 0's stream passes here
+    for (int r = 0; r < ngpus; ++r) {
+        CK(cudaSetDevice(g_rank[r].device));
+        CK(cudaEventRecord(g_rank[r].used, r == 0 ? s0 : g_rank[r].stream));
+    }
+    CK(cudaSetDevice(0));
     // device output without statistics: enqueued only (stream0 orders everything after it)
     if (!stats && !out_host) return MANDEL_OK;
     if (out_host) {
@@ -1048,9 +1092,10 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
             stats->loop_exits += ws[r].exits;
             claims += ws[r].chunks_claimed;
             if (r != 0) transfers += is_dynamic(scheme) ? ws[r].rows_started : 1u;
-            if (scheme == MANDEL_FCFS && ngpus == 1) claims = single_rank_claims(H, opts);
         }
         stats->chunks_claimed = claims;
+        stats->kernel_scheme = scheme;
+        stats->sm_clock_mhz = clock_mhz(ws.data(), ngpus);
         stats->transfers = transfers;
         stats->kernel_launches = (uint32_t)launches;
         stats->ngpus = (uint32_t)ngpus;
@@ -1175,18 +1220,30 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     rc = ensure_rank(0, dev, sbytes, nullptr);
     if (rc) return rc;
     RankCtx& rk = g_rank[0];
+    cudaStream_t s = streamv ? (cudaStream_t)streamv : rk.stream;
+    // MANDEL_KERNEL_REFILL: the per-view EAGER/LAZY choice, probed once per view on this
+    // rank's own device (scratch sample band; cached) -- as mandel_render_ex does
+    KernelChoice kc;
+    const bool auto_k = (!opts || opts->kernel == MANDEL_KERNEL_REFILL) &&
+                        !(scheme == MANDEL_FCFS_MASTER && rank == 0);  // the master computes nothing
+    if (auto_k) {
+        const double bounds[5] = {xmin, xmax, ymin, ymax, R};
+        rc = auto_choice(d, bounds, W, H, iterMax, dtype, opts, rk.state, rk.state_bytes, dev, s, kc);
+        if (rc) return rc;
+    }
     LaunchSpec ls;
     // across processes the counter is (in general) on another GPU: system scope
     rc = build_params(d, W, H, iterMax, dtype, scheme, nranks, rank, opts, out_root, rk.state,
-                      rk.state_bytes, fcfs_counter, nranks > 1, dev, ls);
+                      rk.state_bytes, fcfs_counter, nranks > 1, dev, ls, nullptr, auto_k ? &kc : nullptr);
     if (rc) return rc;
-    cudaStream_t s = streamv ? (cudaStream_t)streamv : rk.stream;
     const double t0 = now_ms();
+    CK(cudaStreamWaitEvent(s, rk.used, 0));  // an earlier enqueued render may still use the state
     CK(cudaMemsetAsync(rk.state, 0, sbytes, s));
     CK(cudaEventRecord(rk.k0, s));
     rc = launch(ls, s);
     if (rc) return rc;
     CK(cudaEventRecord(rk.k1, s));
+    CK(cudaEventRecord(rk.used, s));
     const bool band = opts && opts->band_out;
     if (!stats && !band) return MANDEL_OK;  // asynchronous: enqueued on the stream, not awaited
     mandel::WorkState ws;
@@ -1232,8 +1289,9 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->pixels = ws.pixels;
         stats->warp_iters = ws.warp_iters;
         stats->loop_exits = ws.exits;
-        stats->chunks_claimed = (scheme == MANDEL_FCFS && nranks == 1) ? single_rank_claims(H, opts)
-                                                                      : ws.chunks_claimed;
+        stats->chunks_claimed = ws.chunks_claimed;
+        stats->kernel_scheme = scheme;
+        stats->sm_clock_mhz = clock_mhz(&ws, 1);
         stats->transfers = rank == 0 ? 0u : (is_dynamic(scheme) ? ws.rows_started : 1u);
         stats->kernel_launches = 1;
         stats->ngpus = 1;
@@ -1416,6 +1474,10 @@ void mandel_shutdown(void) {
         if (rc.stream) cudaStreamDestroy(rc.stream);
         if (rc.k0) cudaEventDestroy(rc.k0);
         if (rc.k1) cudaEventDestroy(rc.k1);
+        if (rc.used) {
+            cudaEventSynchronize(rc.used);
+            cudaEventDestroy(rc.used);
+        }
         if (rc.state) cudaFree(rc.state);
         rc = RankCtx();
     }
@@ -1443,6 +1505,13 @@ void mandel_shutdown(void) {
             if (g_root.band_k1[b]) cudaEventDestroy(g_root.band_k1[b]);
             if (g_root.band_cp[b]) cudaEventDestroy(g_root.band_cp[b]);
         }
+    }
+    for (size_t dv = 0; dv < g_dev.size(); ++dv) {
+        if (!g_dev[dv].scratch) continue;
+        cudaSetDevice((int)dv);
+        cudaFree(g_dev[dv].scratch);
+        g_dev[dv].scratch = nullptr;
+        g_dev[dv].scratch_bytes = 0;
     }
     g_root = Root();
     g_auto.clear();

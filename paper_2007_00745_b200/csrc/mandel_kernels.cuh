@@ -64,6 +64,9 @@ struct WorkState {
     unsigned long long pixels;    // pixels stored by this rank
     unsigned long long warp_iters; // inner-loop iterations summed over warps (eager/adaptive)
     unsigned long long exits;      // inner-loop exits summed over warps (eager/adaptive)
+    unsigned long long clk_cycles; // sum over CTAs of thread 0's SM clock cycles (clock64) ...
+    unsigned long long clk_ns;     // ... and of its wall time (%globaltimer): their ratio is the
+                                   // SM clock during the kernel (mandel_stats.sm_clock_mhz)
     // followed by chunk_map[nchunks + 1] (uint32; 0 = unpublished, g+1 = global chunk g,
     // kChunkDone = exhausted)
 };
@@ -418,6 +421,34 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
     return kTileOk;
 }
 
+// The SM clock as the kernel saw it: thread 0 of each CTA reads its SM cycle counter and
+// the global nanosecond timer at start and end; the host divides the sums.
+struct CtaClock {
+    long long c0;
+    unsigned long long t0;
+};
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ CtaClock cta_clock_start() {
+    CtaClock c{0, 0};
+    if (threadIdx.x == 0) {
+        c.t0 = global_ns();
+        c.c0 = clock64();
+    }
+    return c;
+}
+__device__ __forceinline__ void cta_clock_end(const Params& p, const CtaClock& c) {
+    if (threadIdx.x == 0) {
+        const long long c1 = clock64();
+        const unsigned long long t1 = global_ns();
+        atomicAdd(&p.ws->clk_cycles, (unsigned long long)(c1 - c.c0));
+        atomicAdd(&p.ws->clk_ns, t1 - c.t0);
+    }
+}
+
 __device__ __forceinline__ void flush_loop_stats(const Params& p, uint32_t witers, uint32_t exits) {
     if ((threadIdx.x & 31) == 0 && exits) {
         atomicAdd(&p.ws->warp_iters, (unsigned long long)witers);
@@ -623,6 +654,7 @@ template <typename AR, int ILP, int MINB, int BT = 1, bool LSTATS = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
+    const CtaClock clk = cta_clock_start();
     typedef AR A;
     typedef typename AR::T T;
     const unsigned FULL = 0xffffffffu;
@@ -738,6 +770,7 @@ escape_refill_kernel(const Params p) {
     }
     flush_stats(p, my_iters, my_pix);
     if (LSTATS) flush_loop_stats(p, w_iters, w_exits);
+    cta_clock_end(p, clk);
 }
 
 // ---------------------------------------------------------------------------
@@ -793,6 +826,7 @@ template <typename AR, int ILP, int MINB>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_lazy_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
+    const CtaClock clk = cta_clock_start();
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -937,6 +971,7 @@ escape_lazy_kernel(const Params p) {
     }
 #endif
     flush_stats(p, my_iters, my_pix);
+    cta_clock_end(p, clk);
 }
 
 // ---------------------------------------------------------------------------
@@ -961,6 +996,7 @@ template <typename AR, int ILP, int MINB, int BT = 1>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_adaptive_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
+    const CtaClock clk = cta_clock_start();
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -1110,6 +1146,7 @@ escape_adaptive_kernel(const Params p) {
         }
     }
     flush_stats(p, my_iters, my_pix);
+    cta_clock_end(p, clk);
 }
 
 #undef ADAPT_LAZY_STEP_SLOT
@@ -1122,6 +1159,7 @@ escape_adaptive_kernel(const Params p) {
 template <typename AR>
 __global__ void __launch_bounds__(kCtaThreads)
 escape_static_kernel(const Params p) {
+    const CtaClock clk = cta_clock_start();
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -1141,12 +1179,14 @@ escape_static_kernel(const Params p) {
             ++n;
             if (esc) break;
         }
-        p.out[(size_t)row * p.W + j] = n;
+        // band mode (options.band_out): the rank's compact band, band row = its local slot
+        p.out[(size_t)(p.band ? slot : row) * p.W + j] = n;
         my_iters = n;
         my_pix = 1;
         if (threadIdx.x == 0 && j == 0) atomicAdd(&p.ws->rows_started, 1u);
     }
     flush_stats(p, my_iters, my_pix);
+    if (threadIdx.y == 0) cta_clock_end(p, clk);
 }
 
 #undef MANDEL_STEP

@@ -76,6 +76,9 @@ class mandel_stats(ctypes.Structure):
         ("loop_exits", ctypes.c_uint64),
         ("kernel_batch", ctypes.c_int32),
         ("kernel_packed", ctypes.c_int32),
+        ("sm_clock_mhz", ctypes.c_double),
+        ("kernel_scheme", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -95,6 +98,9 @@ class mandel_stats(ctypes.Structure):
             "kernel_ilp": int(self.kernel_ilp), "probe": [float(v) for v in self.probe],
             "warp_iters": int(self.warp_iters), "loop_exits": int(self.loop_exits),
             "kernel_batch": int(self.kernel_batch), "kernel_packed": int(self.kernel_packed),
+            "sm_clock_mhz": float(self.sm_clock_mhz),
+            "kernel_scheme": {v: k for k, v in SCHEMES.items() if k not in ("naive", "alternating")}.get(
+                int(self.kernel_scheme), str(self.kernel_scheme)),
         }
 
 
@@ -217,6 +223,29 @@ def _ptr(a) -> int | None:
     raise TypeError(f"cannot take a pointer of {type(a)}")
 
 
+def _buf(a, nbytes: int, name: str) -> int | None:
+    """_ptr of an output buffer the library writes ``nbytes`` through: numpy arrays and
+    torch tensors must be C-contiguous, have 4-byte elements and hold at least nbytes
+    (a raw integer pointer is the caller's responsibility)."""
+    if a is None or isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        ok_layout = a.flags.c_contiguous and a.flags.writeable
+        item, size = a.itemsize, a.nbytes
+    elif hasattr(a, "data_ptr"):
+        ok_layout = bool(a.is_contiguous())
+        item, size = a.element_size(), a.numel() * a.element_size()
+    else:
+        raise TypeError(f"{name}: cannot take a pointer of {type(a)}")
+    if not ok_layout:
+        raise ValueError(f"{name} must be a C-contiguous, writable buffer")
+    if item != 4:
+        raise ValueError(f"{name} must have 4-byte elements (uint32/int32), not {item}-byte")
+    if size < nbytes:
+        raise ValueError(f"{name} holds {size} bytes; the map needs {nbytes} (W*H*4)")
+    return _ptr(a)
+
+
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
           tile_rows=0, no_pack=False, band_out=False, band_taper=0, max_sms=0, async_host=False):
@@ -261,7 +290,7 @@ def mandel_shutdown() -> None:
 def mandel_render(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme, ngpus, out) -> None:
     """C: mandel_render.  ``out``: host numpy uint32 array (or torch CPU tensor) of W*H."""
     rc = lib().mandel_render(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
-                             _enum(scheme, SCHEMES), ngpus, _ptr(out))
+                             _enum(scheme, SCHEMES), ngpus, _buf(out, W * H * 4, "out"))
     _check(rc, "mandel_render")
 
 
@@ -275,14 +304,16 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict; want_stats=False (device output only)
     enqueues the render on stream0 without waiting and returns None."""
+    need = W * H * 4
+    host_p, dev_p = _buf(out_host, need, "out_host"), _buf(out_dev0, need, "out_dev0")
     st = mandel_stats() if want_stats else None
     o = _opts(chunk_rows=chunk_rows, tile_px=tile_px, kernel=kernel, logical_ranks=logical_ranks,
               refill_lanes=refill_lanes, ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo,
               adapt_hi=adapt_hi, bands=bands, check_every=check_every, tile_rows=tile_rows,
               no_pack=no_pack, band_taper=band_taper, max_sms=max_sms, async_host=async_host)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
-                                _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), _ptr(out_host),
-                                _ptr(out_dev0), stream0, ctypes.byref(st) if st is not None else None)
+                                _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), host_p,
+                                dev_p, stream0, ctypes.byref(st) if st is not None else None)
     _check(rc, "mandel_render_ex")
     return st.as_dict() if st is not None else None
 
@@ -295,6 +326,9 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
     pointers valid in this process (own, or mapped with mandel_ipc_open).
     want_stats=False: the render is only enqueued on ``stream``; returns None."""
+    # out_root: the whole image, or (band_out) this rank's band -- whose row count depends
+    # on the plan, so only the layout is checked for a band
+    root_p = _buf(out_root, 0 if band_out else W * H * 4, "out_root")
     st = mandel_stats() if want_stats else None
     o = _opts(chunk_rows=chunk_rows, tile_px=tile_px, kernel=kernel, refill_lanes=refill_lanes,
               ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo, adapt_hi=adapt_hi,
@@ -302,7 +336,7 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
               max_sms=max_sms)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
-                                  _ptr(out_root), _ptr(fcfs_counter), stream,
+                                  root_p, _ptr(fcfs_counter), stream,
                                   ctypes.byref(st) if st is not None else None)
     _check(rc, "mandel_render_rank")
     return st.as_dict() if st is not None else None

@@ -115,6 +115,25 @@ class RankRenderer:
             self.dist.barrier()
         return st
 
+    def device_barrier(self):
+        """Order every rank's next render after every rank's current one, ON THE DEVICE:
+        a one-element all_reduce enqueued on the render stream (NCCL over NVLink, no host
+        round trip), so a timed sequence of renders measures each render to the moment
+        the last rank's stores have landed in rank 0's map -- the paper's compute time
+        ends when the master holds the image (Eq. 21's T_N),
+        FCFS tail included.  With gloo (the CPU plumbing of the tests) the stream is
+        synchronised and the host barrier used instead."""
+        if self.dist.get_backend() != "nccl":
+            self.M.mandel_sync(self.stream)
+            self.dist.barrier()
+            return
+        import torch
+        dev = torch.device("cuda", self.device)
+        if getattr(self, "_tok", None) is None:
+            self._tok = torch.zeros(1, dtype=torch.int32, device=dev)
+        with torch.cuda.stream(torch.cuda.ExternalStream(self.stream, device=dev)):
+            self.dist.all_reduce(self._tok)
+
     def close(self):
         self.dist.barrier()
         for p in self.mapped:

@@ -43,7 +43,7 @@ def test_library_is_sm100a_only(mandel):
 
 
 def test_abi_version_and_strerror(mandel):
-    assert mandel.mandel_abi_version() == 6
+    assert mandel.mandel_abi_version() == 7
     for code in range(-7, 1):
         assert mandel.strerror(code) and mandel.strerror(code) != "unknown status"
 
@@ -110,3 +110,34 @@ def test_band_api_host_checks(mandel):
     cnt = ctypes.c_uint32(0)
     assert L.mandel_band_rows(None, None) == mandel.MANDEL_EINVAL
     assert L.mandel_band_rows(None, ctypes.byref(cnt)) == mandel.MANDEL_OK and cnt.value == 0
+
+
+def test_binding_validates_output_buffers(mandel):
+    """The binding checks caller buffers before the library writes W*H*4 bytes through
+    them: too small, wrong element size and non-contiguous are rejected
+    with ValueError before any library call."""
+    import torch
+    cfg = wl.C1.with_(W=16, H=12)
+    bad = [np.zeros(cfg.pixels - 1, np.uint32),              # one element short
+           np.zeros(cfg.pixels, np.uint16),                  # 2-byte elements
+           np.zeros((cfg.H, 2 * cfg.W), np.uint32)[:, ::2],  # strided view
+           torch.zeros(cfg.pixels, dtype=torch.float64),     # 8-byte elements
+           torch.zeros((cfg.W, cfg.H), dtype=torch.int32).t()]  # non-contiguous tensor
+    for b in bad:
+        with pytest.raises(ValueError):
+            mandel.mandel_render(*cfg.args(), "fp64", "block", 1, b)
+        with pytest.raises(ValueError):
+            mandel.mandel_render_ex(*cfg.args(), "fp64", "block", 1, out_host=b)
+        with pytest.raises(ValueError):
+            mandel.mandel_render_ex(*cfg.args(), "fp64", "block", 1, out_dev0=b)
+        with pytest.raises(ValueError):
+            mandel.mandel_render_rank(*cfg.args(), "fp64", "block", 0, 1, b)
+    ro = np.zeros(cfg.pixels, np.uint32)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        mandel.mandel_render(*cfg.args(), "fp64", "block", 1, ro)
+    # a correctly sized buffer passes validation (then ENODEV without a device)
+    if mandel.mandel_device_count() == 0:
+        with pytest.raises(mandel.MandelError) as e:
+            mandel.mandel_render(*cfg.args(), "fp64", "block", 1, np.zeros((cfg.H, cfg.W), np.uint32))
+        assert e.value.code == mandel.MANDEL_ENODEV

@@ -117,6 +117,11 @@ def _step_protocol(dist, rank, world):
         want.append(("render", rr.ctr + (n % 3) * B, rr.img))
     want.append(("barrier",))
     ok = ok and steps == want
+    # device_barrier: on the CPU plumbing (gloo) it synchronises the stream, then lines up
+    n1 = len(log)
+    rr.step("block", sync=False)
+    rr.device_barrier()
+    ok = ok and log[n1:] == [("render", rr.ctr + (8 % 3) * B, rr.img), ("sync",), ("barrier",)]
     rr.close()
     return ok
 

@@ -91,11 +91,18 @@ def test_rank_processes_share_one_map(oracle, world, dtype, gather):
         assert iters == int(want.sum(dtype=np.uint64)), (scheme, rep)
 
 
-@pytest.mark.parametrize("scheme", ["block", "cyclic", "fcfs", "fcfs_master"])
+BAND_CASES = [(s, k) for s in ("block", "cyclic", "fcfs", "fcfs_master") for k in ("refill", "lazy2")] + \
+    [("block", "static"), ("cyclic", "static")]
+
+
+@pytest.mark.parametrize("scheme,kernel", BAND_CASES, ids=[f"{s}-{k}" for s, k in BAND_CASES])
 @pytest.mark.parametrize("nranks", [2, 3, 5])
-def test_band_mode_and_scatter(mandel, oracle, scheme, nranks):
+def test_band_mode_and_scatter(mandel, oracle, scheme, kernel, nranks):
     """The NCCL path's device pieces in one process: each rank renders its compact band
-    (band_out), mandel_band_rows lists the band's image rows, K4 places it."""
+    (band_out), mandel_band_rows lists the band's image rows, K4 places it.  The band is
+    sized exactly as the header documents (static: the plan's rows; FCFS: every chunk),
+    so a kernel that stores at image rows instead of band rows writes out of bounds or
+    leaves band rows unwritten (the static kernel did)."""
     import torch
     cfg = wl.C1.with_(W=301, H=203, iter_max=800)
     want = oracle.render(cfg)
@@ -103,14 +110,19 @@ def test_band_mode_and_scatter(mandel, oracle, scheme, nranks):
     stream = torch.cuda.current_stream(dev).cuda_stream
     image = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device=dev)
     ctr = torch.zeros(64, dtype=torch.int32, device=dev)
-    cap = -(-cfg.H // 16) * 16
     chunk = 1 if scheme == "fcfs_master" else 16
-    cap = -(-cfg.H // chunk) * chunk
     seen = []
     for r in range(nranks):
-        band = torch.full((cap, cfg.W), -7, dtype=torch.int32, device=dev)
+        if scheme in ("block", "cyclic"):
+            cap = len(mandel.mandel_plan_rows(scheme, cfg.H, nranks, r))
+        else:
+            cap = -(-cfg.H // chunk) * chunk
+        # one guard row past the documented capacity: it must stay untouched
+        buf = torch.full((cap + 1, cfg.W), -7, dtype=torch.int32, device=dev)
+        band = buf[:cap]
         st = mandel.mandel_render_rank(*cfg.args(), "fp64", scheme, r, nranks, band, ctr, stream,
-                                       band_out=True)
+                                       band_out=True, kernel=kernel)
+        assert bool((buf[cap] == -7).all()), "band_out wrote past the band's capacity"
         rows = mandel.mandel_band_rows()
         if scheme in ("block", "cyclic"):
             assert rows.tolist() == mandel.mandel_plan_rows(scheme, cfg.H, nranks, r).tolist()
@@ -189,3 +201,68 @@ def test_shared_host_image_drain(oracle, world):
     assert got["ok"], got["err"]
     for scheme in ("fcfs", "cyclic"):
         assert np.array_equal(got[scheme], want), scheme
+
+
+def _probe_worker(rank, world, port, cfg, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    from paper_2007_00745_b200 import mandel as M
+    from paper_2007_00745_b200.multiproc import RankRenderer
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        stream = torch.cuda.current_stream(0).cuda_stream
+        rr = RankRenderer(dist, rank, world, 0, cfg.args(), cfg.dtype, stream, slots=4)
+        res = {}
+        for scheme in ("fcfs", "cyclic"):
+            if rank == 0:
+                M.mandel_dev_zero(rr.img, cfg.W * cfg.H * 4, stream)
+            dist.barrier()
+            st = rr.step(scheme, barrier=True)
+            img = None
+            if rank == 0:
+                host = torch.empty((cfg.H, cfg.W), dtype=torch.int32, pin_memory=True)
+                bench._d2h(host, rr.img, cfg.W * cfg.H * 4, stream)
+                img = host.numpy().view(np.uint32).copy()
+            res[scheme] = (st["kernel"], st["probe"][1], img)
+            dist.barrier()
+        rr.close()
+        q.put((rank, res))
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_path_runs_the_view_probe(oracle):
+    """mandel_render_rank makes the same per-view EAGER/LAZY choice as mandel_render_ex
+    (it always ran batched EAGER, ~0.55x of LAZY on C4): on a C4-like zoom
+    every rank process probes on its own device and runs LAZY, and the shared map equals
+    the oracle's."""
+    cfg = wl.C4.with_(W=1536, H=1536, iter_max=5000)
+    want = oracle.render(cfg)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_probe_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0, res
+    for r in range(world):
+        assert isinstance(res[r], dict), res[r]
+        for scheme, (kernel, ipe, _) in res[r].items():
+            assert kernel == "lazy", (r, scheme, kernel, ipe)
+            assert 0 < ipe < 23, (r, scheme, ipe)
+    for scheme, (_, _, img) in res[0].items():
+        bad = int((img != want).sum())
+        assert bad == 0, f"{scheme}: {bad} pixels differ from the oracle"

@@ -297,3 +297,41 @@ def test_fma_map_is_its_own(oracle):
     z = wl.C4.with_(W=512, H=512, iter_max=3000)
     d = int((oracle.render(z) != oracle.render(z.with_(dtype="fp64fma"))).sum())
     assert 0 < d < 512 * 512 // 20
+
+
+# --------------------------------------------------------------------------
+# The threaded row driver (render_rows_mt) -- the checker of every full-size parity
+# test and of the CPU baseline.  It holds no arithmetic of its own; this pins that
+# its row bookkeeping (chunk claims, output placement) returns exactly render_rows'
+# rows, in the order asked, for any thread count and chunk size.
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("threads", [1, 3, 16])
+@pytest.mark.parametrize("chunk", [1, 16])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_render_rows_mt_matches_render_rows(oracle, threads, chunk, dtype):
+    cfg = wl.C1.with_(W=203, H=157, iter_max=400, dtype=dtype)
+    whole = oracle.render(cfg)
+    rng = np.random.default_rng(threads * 100 + chunk)
+    row_sets = {
+        "all": np.arange(cfg.H),
+        "shuffled": rng.permutation(cfg.H),
+        "strided": np.arange(5, cfg.H, 7),
+        "repeated": np.array([3, 3, 156, 0, 77, 3]),
+        "one": np.array([cfg.H - 1]),
+    }
+    for label, rows in row_sets.items():
+        got, used = oracle.render_rows_mt(cfg, rows, threads=threads, chunk=chunk)
+        assert used == threads
+        assert got.shape == (len(rows), cfg.W) and got.dtype == np.uint32
+        for k, r in enumerate(rows):
+            want = oracle.render_rows(*cfg.args(), dtype, int(r), int(r) + 1)[0]
+            assert np.array_equal(got[k], want), (label, k, int(r))
+        assert np.array_equal(got, whole[rows]), label
+
+
+def test_render_rows_mt_empty_and_errors(oracle):
+    cfg = wl.C1.with_(W=50, H=40)
+    got, _ = oracle.render_rows_mt(cfg, np.array([], dtype=np.int64), threads=4)
+    assert got.shape == (0, 50)
+    with pytest.raises(ValueError):  # a row outside [0, H) is rejected, not silently computed
+        oracle.render_rows_mt(cfg, np.array([0, 40]), threads=2)

@@ -76,8 +76,13 @@ def test_c1_all_schemes(mandel, oracle, dtype, scheme, ngpus, kernel):
     assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
     assert st["pixels"] == cfg.pixels
     assert st["kernel_launches"] == ngpus
+    assert st["kernel_scheme"] == scheme  # the row order the kernels ran is the one requested
+    assert 300 < st["sm_clock_mhz"] < 2500, st["sm_clock_mhz"]  # measured in-kernel
     if scheme == "fcfs":
-        assert st["chunks_claimed"] == -(-cfg.H // 16)  # Eq. 19 analog: ceil(H/16) claims
+        # Eq. 19 analog: ceil(H/16) successful claims, counted by the device's claim atomics
+        # (also at N = 1: one claimant still claims every chunk from the counter)
+        assert st["chunks_claimed"] == -(-cfg.H // 16)
+        assert sum(st["rank_rows"]) == cfg.H
     else:
         assert st["transfers"] == ngpus - 1  # Eq. 18 / Eq. 20: T_m = N - 1
         assert st["rank_rows"] == [len(x) for x in (
@@ -261,6 +266,24 @@ def test_fcfs_more_ranks_than_rows(mandel, oracle):
     assert st["chunks_claimed"] == 3
 
 
+@pytest.mark.parametrize("chunk", [1, 5, 16, 0])
+def test_single_rank_fcfs_claims_are_counted(mandel, oracle, chunk):
+    """At N = 1 FCFS really claims: the device counts ceil(H/chunk) successful claims
+    (the count used to be synthesised while the block order ran).  The
+    pipelined host hand-off renders row bands instead and says so (kernel_scheme block,
+    no claims)."""
+    cfg = wl.C1.with_(W=257, H=203, iter_max=500)
+    want = oracle.render(cfg)
+    out, st = _render_dev(mandel, cfg, "fcfs", 1, chunk_rows=chunk)
+    _assert_same(_host(out), want, f"fcfs N=1 chunk={chunk}")
+    c = chunk or 16
+    assert st["chunks_claimed"] == -(-cfg.H // c)
+    assert st["kernel_scheme"] == "fcfs" and st["rank_rows"] == [cfg.H]
+    got, st = mandel.render(*cfg.args(), "fp64", "fcfs", 1, bands=4, chunk_rows=chunk)
+    _assert_same(got, want, "banded")
+    assert st["kernel_scheme"] == "block" and st["chunks_claimed"] == 0 and st["kernel_launches"] == 4
+
+
 def test_host_output_entry_point(mandel, oracle):
     cfg = wl.C1.with_(W=640, H=480)
     out = np.zeros(cfg.pixels, dtype=np.uint32)
@@ -331,6 +354,50 @@ def _properties(oracle, cfg, out, st):
     total = int(out.to(torch.int64).sum())
     assert st["sum_iters"] == total
     assert st["pixels"] == cfg.pixels
+
+
+def _whole_map_check(oracle, cfg, out, band_rows):
+    """Every pixel of the device map ``out`` against the oracle, in row bands (bounded
+    host memory): the oracle renders each band on all host threads (render_rows_mt, pinned
+    to render_rows in test_oracle_pins) while the next band is still on the device.
+    Reports the mismatch count over the whole map and the first mismatching pixel."""
+    bad, first = 0, None
+    for r0 in range(0, cfg.H, band_rows):
+        r1 = min(cfg.H, r0 + band_rows)
+        got = _host(out[r0:r1])
+        want, _ = oracle.render_rows_mt(cfg, np.arange(r0, r1))
+        diff = got != want
+        nb = int(diff.sum())
+        if nb:
+            if first is None:
+                i, j = np.argwhere(diff)[0]
+                first = (r0 + int(i), int(j), int(got[i, j]), int(want[i, j]))
+            bad += nb
+    assert bad == 0, (f"{cfg.name}: {bad} of {cfg.pixels} pixels differ; first at (i, j) = "
+                      f"({first[0]}, {first[1]}): gpu={first[2]} oracle={first[3]}")
+
+
+# The north_star's parity target: bit-exact uint32 maps on all five configs, every pixel
+# (Eq. 2 defines I_{i,j} for each pixel, PAPER.md:31-39).  C1 is whole in the tests above;
+# C2-C5 here, rendered in bench.py's launch configuration (1 GPU, FCFS, default kernel:
+# the per-view EAGER/LAZY choice), plus the other kernel where the oracle is cheap.
+WHOLE = [("C2", "refill"), ("C2", "lazy2"), ("C3", "refill"), ("C4", "refill"), ("C4", "batch8x2"),
+         ("C5", "refill")]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,kernel", WHOLE, ids=[f"{n}-{k}" for n, k in WHOLE])
+def test_full_size_whole_map(mandel, oracle, name, kernel):
+    torch = _torch()
+    cfg = wl.CONFIGS[name]
+    out, st = _render_dev(mandel, cfg, "fcfs", 1, kernel=kernel)
+    _properties(oracle, cfg, out, st)
+    if kernel == "refill":
+        # the per-view choice the bench runs: LAZY on C4's zoom, batched EAGER elsewhere
+        assert st["kernel"] == ("lazy" if name == "C4" else "eager"), st["kernel"]
+    _whole_map_check(oracle, cfg, out, band_rows=2048 if cfg.W <= 16384 else 1024)
+    del out
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.slow
@@ -540,3 +607,54 @@ def test_view_probe_ignores_sm_slicing(mandel, oracle):
     (k0, ipe0), (k1, ipe1) = got
     assert k0 == k1, got
     assert abs(ipe0 - ipe1) <= 0.1 * ipe1, got
+
+
+def test_explicit_ilp_and_budget_honoured(mandel, oracle):
+    """options.ilp / min_ctas apply on top of the per-view kernel choice in both entry
+    points (mandel_render_ex ignored them under MANDEL_KERNEL_REFILL)."""
+    torch = _torch()
+    cfg = wl.C1.with_(W=400, H=300, iter_max=900)
+    want = oracle.render(cfg)
+    for ilp, minb in ((1, 0), (4, 0), (2, 1), (1, 3)):
+        out, st = _render_dev(mandel, cfg, "fcfs", 1, ilp=ilp, min_ctas=minb)
+        _assert_same(_host(out), want, f"ilp={ilp}/min_ctas={minb}")
+        assert st["kernel_ilp"] == ilp, st
+        img = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device="cuda:0")
+        ctr = torch.zeros(4, dtype=torch.int32, device="cuda:0")
+        st = mandel.mandel_render_rank(*cfg.args(), "fp64", "fcfs", 0, 1, img, ctr, None, ilp=ilp, min_ctas=minb)
+        _assert_same(_host(img), want, f"rank ilp={ilp}")
+        assert st["kernel_ilp"] == ilp, st
+
+
+def test_enqueued_renders_on_two_streams(mandel, oracle):
+    """Enqueue-only renders (device output, no statistics) on different streams reuse the
+    library's cached tile counter and rank state; the second must not reset them while
+    the first still draws tiles."""
+    torch = _torch()
+    a = wl.C1.with_(W=1500, H=1400, iter_max=6000)
+    b = wl.C1.with_(W=900, H=700, iter_max=3000, xmin=-2.0, xmax=0.5)
+    wa, wb = oracle.render(a), oracle.render(b)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for rep in range(3):
+        oa = torch.zeros((a.H, a.W), dtype=torch.int32, device="cuda:0")
+        ob = torch.zeros((b.H, b.W), dtype=torch.int32, device="cuda:0")
+        torch.cuda.synchronize()
+        for scheme, n in (("fcfs", 1), ("cyclic", 3))[rep % 2:rep % 2 + 1]:
+            mandel.mandel_render_ex(*a.args(), "fp64", scheme, n, out_dev0=oa, stream0=s1.cuda_stream,
+                                    logical_ranks=n > 1, want_stats=False)
+            mandel.mandel_render_ex(*b.args(), "fp64", scheme, n, out_dev0=ob, stream0=s2.cuda_stream,
+                                    logical_ranks=n > 1, want_stats=False)
+        torch.cuda.synchronize()
+        _assert_same(_host(oa), wa, f"stream 1 rep {rep}")
+        _assert_same(_host(ob), wb, f"stream 2 rep {rep}")
+    # the same through mandel_render_rank (the multi-process entry point)
+    oa = torch.zeros((a.H, a.W), dtype=torch.int32, device="cuda:0")
+    ob = torch.zeros((b.H, b.W), dtype=torch.int32, device="cuda:0")
+    ca = torch.zeros(4, dtype=torch.int32, device="cuda:0")
+    cb = torch.zeros(4, dtype=torch.int32, device="cuda:0")
+    torch.cuda.synchronize()
+    mandel.mandel_render_rank(*a.args(), "fp64", "fcfs", 0, 1, oa, ca, s1.cuda_stream, want_stats=False)
+    mandel.mandel_render_rank(*b.args(), "fp64", "fcfs", 0, 1, ob, cb, s2.cuda_stream, want_stats=False)
+    torch.cuda.synchronize()
+    _assert_same(_host(oa), wa, "rank stream 1")
+    _assert_same(_host(ob), wb, "rank stream 2")

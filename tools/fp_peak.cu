@@ -4,8 +4,13 @@
 //   DADD, DMUL (fp64) and FADD, FMUL (fp32) with 8 independent dependency
 //   chains per thread (no FMA: the escape loop has none), and
 //   the escape-loop body itself (8 FP ops per iteration, no exit test),
-// as lane-operations per second and per SM per cycle (cycles from clock64() on
-// each CTA, averaged).  Prints one JSON object.
+// as lane-operations per second and per SM per cycle.  Cycles come from clock64() on
+// each CTA: the LONGEST CTA span is the kernel's duration in SM cycles (the warp
+// scheduler does not run co-resident CTAs in lockstep -- older warps get priority, so
+// CTAs finish staggered and the MEAN span is only ~56% of the kernel; the r01 output
+// divided the mean span by the kernel time and printed an "implied_mhz" of ~1100 that
+// was this staggering, not the clock).  implied_mhz = longest span / kernel time.
+// Prints one JSON object.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -o tools/fp_peak tools/fp_peak.cu
 #include <cstdio>
@@ -36,7 +41,10 @@ __global__ void __launch_bounds__(256) chains(T seed, int iters, T* sink, unsign
     long long t1 = clock64();
     T s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
     if (s == T(-12345)) sink[0] = s;
-    if (threadIdx.x == 0) atomicAdd(cyc, (unsigned long long)(t1 - t0));
+    if (threadIdx.x == 0) {
+        atomicAdd(&cyc[0], (unsigned long long)(t1 - t0));
+        atomicMax(&cyc[1], (unsigned long long)(t1 - t0));
+    }
 }
 
 // Packed FP32x2 chains (PTX add/mul.rn.f32x2 -> FADD2/FMUL2): 8 packed chains, i.e.
@@ -72,7 +80,10 @@ __global__ void __launch_bounds__(256) chains_f32x2(int iters, float* sink, unsi
         s += lo + hi;
     }
     if (s == -12345.f) sink[0] = s;
-    if (threadIdx.x == 0) atomicAdd(cyc, (unsigned long long)(t1 - t0));
+    if (threadIdx.x == 0) {
+        atomicAdd(&cyc[0], (unsigned long long)(t1 - t0));
+        atomicMax(&cyc[1], (unsigned long long)(t1 - t0));
+    }
 }
 
 // The escape-loop body without the exit test (bounded: c = 0.25i keeps |z| < 1).
@@ -93,7 +104,10 @@ __global__ void __launch_bounds__(256) mandel_body(int iters, T* sink, unsigned 
     }
     long long t1 = clock64();
     if (s == T(-12345) || x == T(-12345)) sink[0] = s + x;
-    if (threadIdx.x == 0) atomicAdd(cyc, (unsigned long long)(t1 - t0));
+    if (threadIdx.x == 0) {
+        atomicAdd(&cyc[0], (unsigned long long)(t1 - t0));
+        atomicMax(&cyc[1], (unsigned long long)(t1 - t0));
+    }
 }
 
 struct Timer {
@@ -101,31 +115,32 @@ struct Timer {
     Timer() { cudaEventCreate(&e0); cudaEventCreate(&e1); }
 };
 
-static void report(const char* name, float ms, unsigned long long cyc, int grid, int sms,
+static void report(const char* name, float ms, const unsigned long long* cyc, int grid, int sms,
                    double ops_per_thread, bool last) {
     double ops = ops_per_thread * 256.0 * grid;
-    double cyc_per_cta = (double)cyc / grid;
+    double mean_span = (double)cyc[0] / grid, max_span = (double)cyc[1];
     int ctas_per_sm = grid / sms;
-    double per_sm_cycle = ops_per_thread * 256.0 * ctas_per_sm / cyc_per_cta;
+    double per_sm_cycle = ops_per_thread * 256.0 * ctas_per_sm / max_span;
     printf("  \"%s\": {\"ms\": %.4f, \"tops\": %.4f, \"lane_ops_per_sm_cycle\": %.2f, "
-           "\"implied_mhz\": %.1f}%s\n", name, ms, ops / (ms * 1e-3) / 1e12, per_sm_cycle,
-           cyc_per_cta / (ms * 1e3), last ? "" : ",");
+           "\"implied_mhz\": %.1f, \"mean_cta_span_frac\": %.3f}%s\n", name, ms,
+           ops / (ms * 1e-3) / 1e12, per_sm_cycle, max_span / (ms * 1e3), mean_span / max_span,
+           last ? "" : ",");
 }
 
 #define BENCH(NAME, KERNEL, ARGS_WARM, ARGS, OPS, LAST)                         \
     do {                                                                        \
-        CK(cudaMemset(cyc, 0, 8));                                              \
+        CK(cudaMemset(cyc, 0, 16));                                             \
         KERNEL<<<grid, 256>>> ARGS_WARM;                                        \
         CK(cudaDeviceSynchronize());                                            \
-        CK(cudaMemset(cyc, 0, 8));                                              \
+        CK(cudaMemset(cyc, 0, 16));                                             \
         cudaEventRecord(t.e0);                                                  \
         KERNEL<<<grid, 256>>> ARGS;                                             \
         cudaEventRecord(t.e1);                                                  \
         CK(cudaDeviceSynchronize());                                            \
         float ms = 0;                                                           \
         cudaEventElapsedTime(&ms, t.e0, t.e1);                                  \
-        unsigned long long c = 0;                                               \
-        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);                         \
+        unsigned long long c[2] = {0, 0};                                       \
+        cudaMemcpy(c, cyc, 16, cudaMemcpyDeviceToHost);                         \
         report(NAME, ms, c, grid, sms, OPS, LAST);                              \
     } while (0)
 
@@ -142,7 +157,7 @@ int main() {
     unsigned long long* cyc;
     CK(cudaMalloc(&dsink, 64));
     CK(cudaMalloc(&fsink, 64));
-    CK(cudaMalloc(&cyc, 8));
+    CK(cudaMalloc(&cyc, 16));
     Timer t;
     printf("{\n  \"sms\": %d, \"ctas_per_sm\": %d, \"threads_per_cta\": 256, \"iters\": %d,\n", sms, occ, it);
     const double chain_ops = (double)it * 32;   // 4 unroll x 8 chains
