@@ -709,6 +709,9 @@ def run_reference(args):
 
 
 def main():
+    import faulthandler
+    import signal
+    faulthandler.register(signal.SIGUSR1, all_threads=True)  # stack dump of a stuck rank on demand
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -133,7 +133,10 @@ typedef struct mandel_stats {
     int32_t  kernel_scheme;        /* the row order the kernels actually ran (enum mandel_scheme):
                                       the requested scheme, except MANDEL_BLOCK for the row bands of
                                       the pipelined one-GPU host hand-off (each band a row range)  */
-    int32_t  reserved0;
+    int32_t  store_mode;           /* how rank 0's kernels stored counts: 0 each count directly (4-B
+                                      stores), 1 staged 8 x 8 blocks stored count by count, 2 staged
+                                      blocks stored with 16-B vector stores (map 16-B aligned, W and
+                                      the tile width multiples of 4)                               */
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
@@ -183,6 +186,13 @@ typedef struct mandel_options {
                                 with the exact per-update test, so counts are unchanged.  Needs
                                 R >= 2 (an escaped orbit then keeps growing); fp32 allows <= 8.
                                 0 -> default (8 when valid, else 1); otherwise MANDEL_EINVAL       */
+    int      stage;          /* output stores (EAGER check-every-8 and LAZY kernels, budgets 1/3):
+                                1 -> staged: each warp collects its 8 x 8 pixel blocks in shared
+                                memory and stores each whole block as 32-B rows with 16-B vector
+                                stores (map 16-B aligned, W a multiple of 4; else count by
+                                count); -1 -> every count stored directly (4-B stores);
+                                0 -> default: staged when the map is on another GPU (the fused
+                                gather's NVLink peer stores), direct into the rank's own HBM    */
 } mandel_options;
 
 /*

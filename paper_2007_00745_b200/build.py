@@ -34,11 +34,32 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def src_hash(define: str = "") -> str:
+    """Content hash of the sources (and the build flags) a library is built from: a copy of
+    the tree with fresh file times (the gpurun snapshot) must not look up to date."""
+    import hashlib
+    h = hashlib.sha1(" ".join(NVCC_FLAGS + [define]).encode())
+    for d in DEPS:
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def _stale(lib: str, define: str = "") -> bool:
+    try:
+        with open(lib + ".srchash") as f:
+            return f.read().strip() != src_hash(define)
+    except OSError:
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def _stamp(lib: str, define: str = "") -> None:
+    with open(lib + ".srchash", "w") as f:
+        f.write(src_hash(define) + "\n")
+
+
+def needs_build() -> bool:
+    return not os.path.exists(LIB) or _stale(LIB)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -53,6 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(LIB + ".tmp", LIB)
+    _stamp(LIB)
     with open(os.path.join(PKG, "ptxas_resources.txt"), "w") as f:
         f.write(res.stderr)
     return LIB
@@ -69,6 +91,16 @@ def build_debug(out: str = None, define: str = "MANDEL_DEBUG_CHECKS=1", name: st
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed building {name}")
+    _stamp(out, define)
+    return out
+
+
+def build_delay(force: bool = False) -> str:
+    """libmandel_delay.so: random sleeps around every FCFS claim, binding and some stores
+    (MANDEL_FCFS_DELAY=1; tests/test_fcfs_stress.py runs it through tools/fcfs_delay_stress.py)."""
+    out = os.path.join(PKG, "libmandel_delay.so")
+    if force or not os.path.exists(out) or _stale(out, "MANDEL_FCFS_DELAY=1"):
+        build_debug(out, "MANDEL_FCFS_DELAY=1", "libmandel_delay.so")
     return out
 
 

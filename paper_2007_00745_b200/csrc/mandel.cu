@@ -236,6 +236,28 @@ int minb_index(int v) {
 #define MANDEL_BT_ROW(T, I, BT) {escape_refill_kernel<T, I, 1, BT>, escape_refill_kernel<T, I, 3, BT>}
 #define MANDEL_BT_ROWS(T, BT) \
     {MANDEL_BT_ROW(T, 1, BT), MANDEL_BT_ROW(T, 2, BT), MANDEL_BT_ROW(T, 3, BT), MANDEL_BT_ROW(T, 4, BT)}
+// Store-staging instantiations (STAGE = true): the batched EAGER loop (check every 8) and
+// LAZY, ILP 1..4 / 1..2, register budgets 1 and 3 CTAs per SM; nullptr otherwise.
+#define MANDEL_BT8S_ROW(T, I) {escape_refill_kernel<T, I, 1, 8, false, true>, escape_refill_kernel<T, I, 3, 8, false, true>}
+#define MANDEL_BT8S_ROWS(T) {MANDEL_BT8S_ROW(T, 1), MANDEL_BT8S_ROW(T, 2), MANDEL_BT8S_ROW(T, 3), MANDEL_BT8S_ROW(T, 4)}
+#define MANDEL_LAZYS_ROWS(T) \
+    {{escape_lazy_kernel<T, 1, 1, true>, escape_lazy_kernel<T, 1, 3, true>}, \
+     {escape_lazy_kernel<T, 2, 1, true>, escape_lazy_kernel<T, 2, 3, true>}}
+KernelFn kernel_fn_staged(int fp32, int variant, int ilp, int mi, int bt) {
+    using namespace mandel;
+    static const KernelFn e8[4][4][2] = {MANDEL_BT8S_ROWS(ArithF64), MANDEL_BT8S_ROWS(ArithF32),
+                                         MANDEL_BT8S_ROWS(ArithF64Fma), MANDEL_BT8S_ROWS(ArithF32P)};
+    static const KernelFn lz[3][2][2] = {MANDEL_LAZYS_ROWS(ArithF64), MANDEL_LAZYS_ROWS(ArithF32),
+                                         MANDEL_LAZYS_ROWS(ArithF64Fma)};
+    if (mi < 0 || mi > 5) return nullptr;
+    const int bi = kMinbVals[mi] == 1 ? 0 : (kMinbVals[mi] == 3 ? 1 : -1);
+    if (bi < 0 || fp32 < 0 || fp32 > 3) return nullptr;
+    if (variant == MANDEL_KERNEL_EAGER && bt == 8 && ilp >= 1 && ilp <= 4) return e8[fp32][ilp - 1][bi];
+    if (fp32 == 3) fp32 = 1;
+    if (variant == MANDEL_KERNEL_LAZY && ilp >= 1 && ilp <= 2) return lz[fp32][ilp - 1][bi];
+    return nullptr;
+}
+
 KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
     using namespace mandel;
     static const KernelFn eager[3][4][6] = {MANDEL_ILP4_ROWS(escape_refill_kernel, ArithF64),
@@ -419,7 +441,7 @@ uint32_t effective_chunk(int scheme, const mandel_options* o) {
 int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype, int scheme,
                  int nranks, int rank, const mandel_options* o, uint32_t* out, void* state,
                  size_t state_cap, uint32_t* fcfs_ctr, bool fcfs_sys, int device, LaunchSpec& ls,
-                 const Plan* band = nullptr, const KernelChoice* force = nullptr) {
+                 const Plan* band = nullptr, const KernelChoice* force = nullptr, bool remote = false) {
     // FCFS runs its claims even with a single claimant (the counter then hands out chunks
     // 0, 1, 2, ... in order; chunks_claimed is the device's own count, Eq. 19).
     // FCFS_MASTER: rank 0 computes nothing (an empty plan, its kernel exits at once);
@@ -545,9 +567,22 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
                         kc.ilp >= 2 && !(o && o->no_pack);
     kc.packed = packed ? 1 : 0;
     ls.kc = kc;
-    ls.fn = kernel_fn(packed ? 3 : fi, kc.variant, kc.ilp, mi, kc.bt);
+    // store staging (options.stage; DESIGN.md §6 "Store staging"): staged 8 x 8 blocks stored
+    // with 16-B vector stores.  Default: staged when the map is another GPU's (the fused
+    // gather's peer stores cross NVLink), direct 4-B stores into local HBM, where the L2
+    // already merges them into whole lines (staging costs 1-4% there, measured)
+    const int so = o ? o->stage : 0;
+    if (so < -1 || so > 1) return fail(MANDEL_EINVAL, "options.stage must be -1, 0 or 1");
+    bool stage = so == 1 || (so == 0 && remote);
+    ls.fn = stage ? kernel_fn_staged(packed ? 3 : fi, kc.variant, kc.ilp, mi, kc.bt) : nullptr;
+    if (!ls.fn) {  // no staged instantiation of this variant: direct stores
+        stage = false;
+        ls.fn = kernel_fn(packed ? 3 : fi, kc.variant, kc.ilp, mi, kc.bt);
+    }
     p.opaque_zero = 0u;
     p.band = (o && o->band_out) ? 1u : 0u;
+    p.stage = stage ? 1u : 0u;
+    p.vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0 && (W & 3u) == 0 && (tile & 3u) == 0) ? 1u : 0u;
     p.out_rows = p.band ? 0u : H;  // a band's capacity is the caller's (not known here)
     if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
     const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;  // (the probe variant is persistent)
@@ -578,6 +613,19 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     }
     return MANDEL_OK;
 }
+
+// true when ptr is memory of device dev (a pointer another process mapped with CUDA IPC
+// reports the device that owns the memory)
+bool same_device(const void* ptr, int dev) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice && a.device == dev;
+}
+
+int store_mode(const mandel::Params& p) { return p.stage ? (p.vec_ok ? 2 : 1) : 0; }
 
 // SM clock over a set of kernel states (mandel_stats.sm_clock_mhz): sum of cycles / sum of ns
 double clock_mhz(const mandel::WorkState* ws, int n) {
@@ -900,6 +948,7 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         stats->kernel_ilp = specs[0].kc.ilp;
         stats->kernel_batch = specs[0].kc.bt;
         stats->kernel_packed = specs[0].kc.packed;
+        stats->store_mode = store_mode(specs[0].p);
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -1006,7 +1055,8 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         rc = ensure_rank(r, dev, sbytes, nullptr);
         if (rc) return rc;
         rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, g_rank[r].state,
-                          g_rank[r].state_bytes, g_root.fcfs_ctr, nphys > 1, dev, specs[r], nullptr, kcp);
+                          g_rank[r].state_bytes, g_root.fcfs_ctr, nphys > 1, dev, specs[r], nullptr, kcp,
+                          dev != 0);
         if (rc) return rc;
     }
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
@@ -1104,6 +1154,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         stats->kernel_ilp = specs[0].kc.ilp;
         stats->kernel_batch = specs[0].kc.bt;
         stats->kernel_packed = specs[0].kc.packed;
+        stats->store_mode = store_mode(specs[0].p);
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -1233,8 +1284,11 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     }
     LaunchSpec ls;
     // across processes the counter is (in general) on another GPU: system scope
+    // the fused gather: a rank other than 0 stores into rank 0's map on another GPU (its
+    // band, with options.band_out, is local)
+    const bool remote = rank != 0 && !(opts && opts->band_out) && !same_device(out_root, dev);
     rc = build_params(d, W, H, iterMax, dtype, scheme, nranks, rank, opts, out_root, rk.state,
-                      rk.state_bytes, fcfs_counter, nranks > 1, dev, ls, nullptr, auto_k ? &kc : nullptr);
+                      rk.state_bytes, fcfs_counter, nranks > 1, dev, ls, nullptr, auto_k ? &kc : nullptr, remote);
     if (rc) return rc;
     const double t0 = now_ms();
     CK(cudaStreamWaitEvent(s, rk.used, 0));  // an earlier enqueued render may still use the state
@@ -1300,6 +1354,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->kernel_ilp = ls.kc.ilp;
         stats->kernel_batch = ls.kc.bt;
         stats->kernel_packed = ls.kc.packed;
+        stats->store_mode = store_mode(ls.p);
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t0;

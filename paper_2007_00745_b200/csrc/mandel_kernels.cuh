@@ -43,6 +43,27 @@ namespace mandel {
         }                                                                                   \
     } while (0)
 
+// FCFS stress build (-DMANDEL_FCFS_DELAY=1 -> libmandel_delay.so, tests only): random
+// sleeps before each claim, between a claim and its binding, at rank start and before
+// some stores, so the claim protocol runs under adversarial interleavings (SPEC.md:281
+// "injected adversarial per-row delays").
+#ifndef MANDEL_FCFS_DELAY
+#define MANDEL_FCFS_DELAY 0
+#endif
+__device__ __forceinline__ void fcfs_delay(uint32_t salt, uint32_t odds_log2 = 1) {
+#if MANDEL_FCFS_DELAY
+    uint32_t h = salt * 0x9E3779B1u ^ (uint32_t)clock64() ^ (blockIdx.x * 0x85EBCA6Bu) ^
+                 (threadIdx.x * 0xC2B2AE35u);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if ((h & ((1u << odds_log2) - 1u)) == 0) __nanosleep((h >> 12) & 0x3FFFu);  // up to ~16 us
+#else
+    (void)salt;
+    (void)odds_log2;
+#endif
+}
+
 #ifndef MANDEL_LAZY_UNROLL
 #define MANDEL_LAZY_UNROLL 16
 #endif
@@ -85,6 +106,8 @@ struct Params {
     uint32_t opaque_zero;            // 0: ArithF32P's contraction barrier (XOR operand)
     uint32_t band;                   // 1: out is this rank's compact band (row = local slot)
     uint32_t out_rows;               // rows the out buffer holds (debug checks; H for the image)
+    uint32_t stage;                  // 1: stores go through the per-warp staging ring (StageEntry)
+    uint32_t vec_ok;                 // 1: out, W and tile_w allow 16-B stores of 4 counts
     // static schemes: slot s -> row s < count0 ? base0 + s*stride0 : base1 + (s - count0)
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
@@ -312,6 +335,7 @@ enum : int { kTileOk = 0, kTileSkip = 1, kTileNone = 2 };
 // GPUs claim from it too (NVLink), device scope otherwise.  Returns the chunk_map
 // entry: global chunk + 1, or kChunkDone once every chunk is taken.
 __device__ __forceinline__ uint32_t claim_chunk(const Params& p) {
+    fcfs_delay(1);
     const uint32_t c = p.fcfs_sys ? atomicAdd_system(p.fcfs_ctr, 1u) : atomicAdd(p.fcfs_ctr, 1u);
     if (c < p.nchunks) {
         atomicAdd(&p.ws->chunks_claimed, 1u);
@@ -350,11 +374,11 @@ __device__ __forceinline__ Tile bcast_tile(const Tile& t) {
 // Pixel q of tile t -> image (row, col) and the row of the output buffer it is stored
 // to: the image row, or (band mode) the rank-local band row = its local slot.
 __device__ __forceinline__ void tile_pixel(const Params& p, const Tile& t, uint32_t q, uint32_t& row,
-                                           uint32_t& col, uint32_t& orow) {
+                                           uint32_t& col, uint32_t& orow, uint32_t& sub, uint32_t& w) {
     // full groups (the common case) have a power-of-two height: shift instead of divide
     const uint32_t band = t.nrows << 3;
-    const uint32_t sub = t.nrows == p.tile_rows ? q >> p.tile_shift : q / band;
-    const uint32_t w = q - sub * band;
+    sub = t.nrows == p.tile_rows ? q >> p.tile_shift : q / band;
+    w = q - sub * band;
     const uint32_t bw = min(8u, t.cols - (sub << 3));
     uint32_t dy, dx;
     if (bw == 8u) {
@@ -371,6 +395,133 @@ __device__ __forceinline__ void tile_pixel(const Params& p, const Tile& t, uint3
                                   : (sl < p.count0 ? p.base0 + sl * p.stride0 : p.base1 + (sl - p.count0));
     orow = p.band ? t.slot + dy : row;
     MANDEL_DCHECK(row < p.H && (p.out_rows == 0 || orow < p.out_rows));
+}
+__device__ __forceinline__ void tile_pixel(const Params& p, const Tile& t, uint32_t q, uint32_t& row,
+                                           uint32_t& col, uint32_t& orow) {
+    uint32_t sub, w;
+    tile_pixel(p, t, q, row, col, orow, sub, w);
+}
+
+// ---------------------------------------------------------------------------
+// Store staging (a5, and a6 when out is rank 0's peer-mapped map): coalesced,
+// vectorised output stores.  A warp hands its tile stream out in blocks -- the 8-column
+// sub-blocks of tile_pixel, up to 8 rows x 8 columns.  Each block in flight owns an
+// entry of a per-warp ring of kStageEntries in shared memory, zeroed when opened; a
+// retiring slot writes its count there (one STS instead of the scattered 4-B global
+// store).  When the stream needs the entry again, kStageEntries blocks later, the block
+// is stored: if every count is there (all nonzero -- counts are >= 1) as whole 32-B rows,
+// two lanes per row with one 16-B vector store each (STG.E.128); otherwise (a slow
+// interior pixel still computing) its retired counts one by one, and the slots still
+// computing its pixels switch to direct stores (kStageDirect).  No atomics: nothing is
+// tracked per retirement.  The warp stores what is left in its ring when it ends.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kStageEntries = 8;
+constexpr uint32_t kStageDirect = 0xffffffffu;
+
+struct __align__(16) StageEntry {
+    uint32_t npx;             // pixels of the block; 0 = the entry is free
+    uint32_t base, slot;      // the tile's base (tile_pixel) and first band slot
+    uint32_t col0;            // first image column of the block
+    uint32_t shape;           // rows | columns << 8
+    uint32_t pad[3];
+    uint32_t counts[64];      // row-major inside the block (tile_pixel's w); 0 = not retired
+};
+
+__device__ __forceinline__ uint32_t stage_orow(const Params& p, uint32_t base, uint32_t slot, uint32_t dy) {
+    const uint32_t sl = base + dy;
+    const uint32_t row = p.scheme == kSchemeFcfs ? sl
+                                                 : (sl < p.count0 ? p.base0 + sl * p.stride0 : p.base1 + (sl - p.count0));
+    const uint32_t orow = p.band ? slot + dy : row;
+    MANDEL_DCHECK(row < p.H && (p.out_rows == 0 || orow < p.out_rows));
+    return orow;
+}
+
+// Store the retired counts of an open entry (warp-collective, warp-uniform en) and free
+// it.  Returns true when the block was complete.
+__device__ __forceinline__ bool stage_store(const Params& p, StageEntry& en, uint32_t lane) {
+    __syncwarp();  // every lane's count is in shared memory
+    const uint32_t nr = en.shape & 0xffu, bw = en.shape >> 8;
+    const unsigned FULL = 0xffffffffu;
+    bool whole = false;
+    if (bw == 8u && p.vec_ok) {
+        // lane 2*dy + h holds columns 4h..4h+3 of row dy: counts[4*lane .. 4*lane + 3]
+        const bool mine = lane < 2 * nr;
+        uint4 v = make_uint4(1u, 1u, 1u, 1u);
+        if (mine) v = *reinterpret_cast<const uint4*>(&en.counts[4 * lane]);
+        whole = __all_sync(FULL, v.x != 0u && v.y != 0u && v.z != 0u && v.w != 0u);
+        if (whole && mine) {
+            const uint32_t dy = lane >> 1, h = lane & 1u;
+            uint32_t* dst = p.out + ((size_t)stage_orow(p, en.base, en.slot, dy) * p.W + en.col0 + h * 4);
+            MANDEL_DCHECK((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+            *reinterpret_cast<uint4*>(dst) = v;
+        }
+    }
+    if (!whole) {
+        // narrow edge blocks, misaligned maps and incomplete blocks: count by count, row-major
+        bool all = true;
+        for (uint32_t w = lane; w < nr * bw; w += 32) {
+            const uint32_t n = en.counts[w];
+            if (n != 0u) {
+                const uint32_t dy = w / bw, dx = w - dy * bw;
+                MANDEL_DCHECK(en.col0 + dx < p.W && n <= p.iter_max);
+                p.out[(size_t)stage_orow(p, en.base, en.slot, dy) * p.W + en.col0 + dx] = n;
+            } else {
+                all = false;
+            }
+        }
+        whole = __all_sync(FULL, all);
+    }
+    __syncwarp();
+    if (lane == 0) en.npx = 0u;
+    __syncwarp();
+    return whole;
+}
+
+// Open ring entry e for sub-block `sub` of tile t (warp-uniform).  The block still in the
+// entry is stored first; if it was incomplete, the slots computing its pixels (tag entry
+// e) switch to direct stores -- their global address is formed here from the entry (a
+// staged slot never needs it otherwise).
+template <int ILP>
+__device__ __forceinline__ void stage_open(const Params& p, StageEntry* ring, uint32_t e, const Tile& t,
+                                           uint32_t sub, uint32_t lane, uint32_t (&stag)[ILP],
+                                           uint32_t* (&dst)[ILP]) {
+    StageEntry& en = ring[e];
+    if (en.npx != 0u && !stage_store(p, en, lane)) {
+        const uint32_t bw = en.shape >> 8;
+#pragma unroll
+        for (int s = 0; s < ILP; ++s) {
+            if (stag[s] != kStageDirect && (stag[s] >> 6) == e) {
+                const uint32_t w = stag[s] & 63u, dy = w / bw, dx = w - dy * bw;
+                dst[s] = p.out + ((size_t)stage_orow(p, en.base, en.slot, dy) * p.W + en.col0 + dx);
+                stag[s] = kStageDirect;
+            }
+        }
+    }
+    if (lane < 16) *reinterpret_cast<uint4*>(&en.counts[lane * 4]) = make_uint4(0u, 0u, 0u, 0u);
+    if (lane == 0) {
+        const uint32_t bw = min(8u, t.cols - (sub << 3));
+        en.npx = t.nrows * bw;
+        en.base = t.base;
+        en.slot = t.slot;
+        en.col0 = t.j0 + (sub << 3);
+        en.shape = t.nrows | (bw << 8);
+    }
+    __syncwarp();
+}
+
+// A slot retires count n: into its block's entry, or directly when it is not staged.
+__device__ __forceinline__ void stage_retire(StageEntry* ring, uint32_t tag, uint32_t* dst, uint32_t n) {
+    if (tag == kStageDirect) *dst = n;
+    else ring[tag >> 6].counts[tag & 63u] = n;
+}
+
+// At the warp's end: store every block still in the ring (all complete by then, except
+// blocks some of whose pixels were handed out unstaged).
+__device__ __forceinline__ void stage_drain(const Params& p, StageEntry* ring, uint32_t lane) {
+    __syncwarp();
+#pragma unroll 1
+    for (uint32_t e = 0; e < kStageEntries; ++e)
+        if (ring[e].npx != 0u) stage_store(p, ring[e], lane);
 }
 
 // (ck, cg) caches lane 0's last local->global chunk binding, so only the first
@@ -401,10 +552,17 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
             // first tile of local chunk k: bind chunk 0 if k == 0, then bind chunk k+1 one
             // chunk ahead (claims stay in local-chunk order; chunk k is already bound when
             // its first tile is drawn, so warps rarely wait on a claim in flight)
-            if (k == 0) st_volatile(&p.chunk_map[0], claim_chunk(p));
+            if (k == 0) {
+                const uint32_t g0 = claim_chunk(p);
+                fcfs_delay(2);
+                st_volatile(&p.chunk_map[0], g0);
+            }
             g = wait_bound(p, k);
-            if (k + 1 <= p.nchunks)
-                st_volatile(&p.chunk_map[k + 1], g == kChunkDone ? kChunkDone : claim_chunk(p));
+            if (k + 1 <= p.nchunks) {
+                const uint32_t gn = g == kChunkDone ? kChunkDone : claim_chunk(p);
+                fcfs_delay(3);  // the claim is made, its binding not yet visible
+                st_volatile(&p.chunk_map[k + 1], gn);
+            }
         } else {
             g = wait_bound(p, k);
         }
@@ -422,32 +580,31 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
 }
 
 // The SM clock as the kernel saw it: thread 0 of each CTA reads its SM cycle counter and
-// the global nanosecond timer at start and end; the host divides the sums.
-struct CtaClock {
-    long long c0;
-    unsigned long long t0;
-};
+// the global nanosecond timer at start and end (kept in shared memory, not registers);
+// the host divides the sums.
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ CtaClock cta_clock_start() {
-    CtaClock c{0, 0};
-    if (threadIdx.x == 0) {
-        c.t0 = global_ns();
-        c.c0 = clock64();
+__device__ __forceinline__ void cta_clock_start(unsigned long long* sm) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        sm[1] = global_ns();
+        sm[0] = (unsigned long long)clock64();
     }
-    return c;
 }
-__device__ __forceinline__ void cta_clock_end(const Params& p, const CtaClock& c) {
-    if (threadIdx.x == 0) {
+__device__ __forceinline__ void cta_clock_end(const Params& p, const unsigned long long* sm) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
         const long long c1 = clock64();
         const unsigned long long t1 = global_ns();
-        atomicAdd(&p.ws->clk_cycles, (unsigned long long)(c1 - c.c0));
-        atomicAdd(&p.ws->clk_ns, t1 - c.t0);
+        atomicAdd(&p.ws->clk_cycles, (unsigned long long)c1 - sm[0]);
+        atomicAdd(&p.ws->clk_ns, t1 - sm[1]);
     }
 }
+#define MANDEL_CTA_CLOCK_START()                       \
+    __shared__ unsigned long long mandel_clk_sm_[2];   \
+    cta_clock_start(mandel_clk_sm_)
+#define MANDEL_CTA_CLOCK_END() cta_clock_end(p, mandel_clk_sm_)
 
 __device__ __forceinline__ void flush_loop_stats(const Params& p, uint32_t witers, uint32_t exits) {
     if ((threadIdx.x & 31) == 0 && exits) {
@@ -650,11 +807,13 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
 // ---------------------------------------------------------------------------
 // LSTATS: count loop exits and iterations per warp (the kernel-choice probe only:
 // the two counters cost ~3% on C2 in production, measured A/B).
-template <typename AR, int ILP, int MINB, int BT = 1, bool LSTATS = false>
+// STAGE: stores go through the per-warp staging ring (the instantiation the host picks
+// when p.stage is set; without it the kernel keeps no staging state at all).
+template <typename AR, int ILP, int MINB, int BT = 1, bool LSTATS = false, bool STAGE = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
-    const CtaClock clk = cta_clock_start();
+    MANDEL_CTA_CLOCK_START();
     typedef AR A;
     typedef typename AR::T T;
     const unsigned FULL = 0xffffffffu;
@@ -667,20 +826,30 @@ escape_refill_kernel(const Params p) {
     T x[ILP], y[ILP], x2[ILP], y2[ILP], cr[ILP], ci[ILP];
     uint32_t rem[ILP];
     uint32_t* dst[ILP];
+    uint32_t stag[ILP];  // the slot's staging tag (entry * 64 + pixel of the block) or kStageDirect
 #pragma unroll
     for (int s = 0; s < ILP; ++s) {
         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
         rem[s] = kIdleRem;
         dst[s] = p.out;
+        stag[s] = kStageDirect;
     }
     unsigned long long my_iters = 0, my_pix = 0;
     uint32_t w_iters = 0, w_exits = 0;  // warp-uniform loop statistics (wrap-free below 2^32)
+
+    // this warp's store-staging ring (StageEntry)
+    __shared__ StageEntry stage_ring[STAGE ? kWarpsPerCta : 1][STAGE ? kStageEntries : 1];
+    StageEntry* const ring = stage_ring[STAGE ? threadIdx.x >> 5 : 0];
+    if (STAGE && lane < kStageEntries) ring[lane].npx = 0u;
+    __syncwarp();
+    uint32_t tile_e0 = 0, sub_open = 0;  // ring entry of the tile's sub-block 0; sub-blocks opened
 
     // warp-uniform tile cursor: pixels [tq, tqend) of tile tl
     Tile tl = {0u, 0u, 0u, 0u, 0u};
     uint32_t tq = 0, tqend = 0;
     bool more = true;
     uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
+    fcfs_delay(4);
     unsigned need[ILP];
 #pragma unroll
     for (int s = 0; s < ILP; ++s) need[s] = FULL;
@@ -695,6 +864,8 @@ escape_refill_kernel(const Params p) {
         }
         if (nd) {
             uint32_t served = 0;
+            uint32_t opens = 0;  // ring entries opened this round: at most kStageEntries - 1, so
+                                 // the blocks one round hands out never share an entry
             for (;;) {
                 if (tq >= tqend) {
                     if (!more) break;
@@ -706,19 +877,31 @@ escape_refill_kernel(const Params p) {
                     tl = bcast_tile(tl);
                     tq = 0;
                     tqend = tl.nrows * tl.cols;
+                    tile_e0 = (tile_e0 + sub_open) & (kStageEntries - 1);
+                    sub_open = 0;
                 }
                 const uint32_t take = min(tqend - tq, nd - served);
+                if (STAGE) {
+                    // open the ring entries of the sub-blocks this round hands out (pixels of a
+                    // sub-block left unopened -- tiny blocks only -- store directly)
+                    const uint32_t qe = tq + take - 1;
+                    const uint32_t last = tl.nrows == p.tile_rows ? qe >> p.tile_shift : qe / (tl.nrows << 3);
+                    for (; sub_open <= last && opens < kStageEntries - 1; ++sub_open, ++opens)
+                        stage_open<ILP>(p, ring, (tile_e0 + sub_open) & (kStageEntries - 1), tl, sub_open, lane, stag, dst);
+                }
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
                     const uint32_t q = rank[s] - served;
                     if (((need[s] >> lane) & 1u) && q < take) {
-                        uint32_t i, j, o;
-                        tile_pixel(p, tl, tq + q, i, j, o);
+                        uint32_t i, j, o, sb, w;
+                        tile_pixel(p, tl, tq + q, i, j, o, sb, w);
                         cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
                         ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
                         x[s] = y[s] = x2[s] = y2[s] = zero;
                         rem[s] = p.iter_max;
-                        dst[s] = p.out + ((size_t)o * p.W + j);
+                        const bool stg = STAGE && sb < sub_open;
+                        stag[s] = stg ? ((((tile_e0 + sb) & (kStageEntries - 1)) << 6) | w) : kStageDirect;
+                        if (!stg) dst[s] = p.out + ((size_t)o * p.W + j);
                     }
                 }
                 tq += take;
@@ -751,7 +934,8 @@ escape_refill_kernel(const Params p) {
             w_exits += 1;
         }
 
-        // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image)
+        // ---- retire finished slots (a5, +a6 when dst is rank 0's peer image): into the
+        // staging ring, completed blocks stored whole with vector stores
 #pragma unroll
         for (int s = 0; s < ILP; ++s) {
             bool done = false;
@@ -761,16 +945,19 @@ escape_refill_kernel(const Params p) {
             }
             if (done) {
                 const uint32_t n = p.iter_max - rem[s];
-                *dst[s] = n;
+                fcfs_delay(5, 5);
+                if (STAGE) stage_retire(ring, stag[s], dst[s], n);
+                else *dst[s] = n;
                 my_iters += n;
                 my_pix += 1;
             }
             need[s] = __ballot_sync(FULL, done);
         }
     }
+    if (STAGE) stage_drain(p, ring, lane);
     flush_stats(p, my_iters, my_pix);
     if (LSTATS) flush_loop_stats(p, w_iters, w_exits);
-    cta_clock_end(p, clk);
+    MANDEL_CTA_CLOCK_END();
 }
 
 // ---------------------------------------------------------------------------
@@ -822,11 +1009,11 @@ __device__ unsigned long long g_lazy_prof[8];
 __device__ unsigned int g_lazy_prof_done;
 #endif
 
-template <typename AR, int ILP, int MINB>
+template <typename AR, int ILP, int MINB, bool STAGE = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_lazy_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
-    const CtaClock clk = cta_clock_start();
+    MANDEL_CTA_CLOCK_START();
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -844,13 +1031,20 @@ escape_lazy_kernel(const Params p) {
     bool live[ILP];  // the slot's pixel has not finished (its count still advances)
     bool has[ILP];   // the slot holds a pixel not yet stored (else idle: z = c = 0)
     uint32_t* dst[ILP];
+    uint32_t stag[ILP];  // staging tag (as escape_refill_kernel)
 #pragma unroll
     for (int s = 0; s < ILP; ++s) {
         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
         n[s] = 0;
         live[s] = has[s] = false;
         dst[s] = p.out;
+        stag[s] = kStageDirect;
     }
+    __shared__ StageEntry stage_ring[STAGE ? kWarpsPerCta : 1][STAGE ? kStageEntries : 1];
+    StageEntry* const ring = stage_ring[STAGE ? threadIdx.x >> 5 : 0];
+    if (STAGE && lane < kStageEntries) ring[lane].npx = 0u;
+    __syncwarp();
+    uint32_t tile_e0 = 0, sub_open = 0;
     unsigned long long my_iters = 0, my_pix = 0;
     Tile tl = {0u, 0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
     uint32_t tq = 0, tqend = 0;
@@ -859,6 +1053,7 @@ escape_lazy_kernel(const Params p) {
 #if MANDEL_LAZY_PROF
     unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
+    fcfs_delay(4);
 
     for (;;) {
         // ---- refill free slots from the warp's tile stream
@@ -871,6 +1066,7 @@ escape_lazy_kernel(const Params p) {
             nd += __popc(need[s]);
         }
         uint32_t served = 0;
+        uint32_t opens = 0;  // ring entries opened this round (see escape_refill_kernel)
         while (served < nd) {
             if (tq >= tqend) {
                 if (!more) break;
@@ -882,19 +1078,29 @@ escape_lazy_kernel(const Params p) {
                 tl = bcast_tile(tl);
                 tq = 0;
                 tqend = tl.nrows * tl.cols;
+                tile_e0 = (tile_e0 + sub_open) & (kStageEntries - 1);
+                sub_open = 0;
             }
             const uint32_t take = min(tqend - tq, nd - served);
+            if (STAGE) {
+                const uint32_t qe = tq + take - 1;
+                const uint32_t last = tl.nrows == p.tile_rows ? qe >> p.tile_shift : qe / (tl.nrows << 3);
+                for (; sub_open <= last && opens < kStageEntries - 1; ++sub_open, ++opens)
+                    stage_open<ILP>(p, ring, (tile_e0 + sub_open) & (kStageEntries - 1), tl, sub_open, lane, stag, dst);
+            }
 #pragma unroll
             for (int s = 0; s < ILP; ++s) {
                 if (((need[s] >> lane) & 1u) && rank[s] >= served && rank[s] < served + take) {
-                    uint32_t i, j, o;
-                    tile_pixel(p, tl, tq + (rank[s] - served), i, j, o);
+                    uint32_t i, j, o, sb, w;
+                    tile_pixel(p, tl, tq + (rank[s] - served), i, j, o, sb, w);
                     cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));  // Cx[j] = xmin + j*dx
                     ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));  // Cy[i] = ymax - i*dy
                     x[s] = y[s] = x2[s] = y2[s] = zero;
                     n[s] = 0;
                     live[s] = has[s] = true;
-                    dst[s] = p.out + ((size_t)o * p.W + j);
+                    const bool stg = STAGE && sb < sub_open;
+                    stag[s] = stg ? ((((tile_e0 + sb) & (kStageEntries - 1)) << 6) | w) : kStageDirect;
+                    if (!stg) dst[s] = p.out + ((size_t)o * p.W + j);
                 }
             }
             tq += take;
@@ -939,11 +1145,14 @@ escape_lazy_kernel(const Params p) {
             }
         }
 
-        // ---- retire the finished slots (a5, +a6 when dst is rank 0's peer image)
+        // ---- retire the finished slots (a5, +a6 when dst is rank 0's peer image) through
+        // the staging ring (escape_refill_kernel)
 #pragma unroll
         for (int s = 0; s < ILP; ++s) {
             if (has[s] && !live[s]) {
-                *dst[s] = n[s];
+                fcfs_delay(5, 5);
+                if (STAGE) stage_retire(ring, stag[s], dst[s], n[s]);
+                else *dst[s] = n[s];
                 my_iters += n[s];
                 my_pix += 1;
                 has[s] = false;
@@ -951,6 +1160,7 @@ escape_lazy_kernel(const Params p) {
             }
         }
     }
+    if (STAGE) stage_drain(p, ring, lane);
 #if MANDEL_LAZY_PROF
     for (int q = 0; q < 8; ++q) {
         unsigned long long v = q < 6 ? prof[q] : (lane == 0 ? prof[q] : 0ull);
@@ -971,7 +1181,7 @@ escape_lazy_kernel(const Params p) {
     }
 #endif
     flush_stats(p, my_iters, my_pix);
-    cta_clock_end(p, clk);
+    MANDEL_CTA_CLOCK_END();
 }
 
 // ---------------------------------------------------------------------------
@@ -996,7 +1206,7 @@ template <typename AR, int ILP, int MINB, int BT = 1>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_adaptive_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
-    const CtaClock clk = cta_clock_start();
+    MANDEL_CTA_CLOCK_START();
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -1146,7 +1356,7 @@ escape_adaptive_kernel(const Params p) {
         }
     }
     flush_stats(p, my_iters, my_pix);
-    cta_clock_end(p, clk);
+    MANDEL_CTA_CLOCK_END();
 }
 
 #undef ADAPT_LAZY_STEP_SLOT
@@ -1159,7 +1369,7 @@ escape_adaptive_kernel(const Params p) {
 template <typename AR>
 __global__ void __launch_bounds__(kCtaThreads)
 escape_static_kernel(const Params p) {
-    const CtaClock clk = cta_clock_start();
+    MANDEL_CTA_CLOCK_START();
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -1186,7 +1396,7 @@ escape_static_kernel(const Params p) {
         if (threadIdx.x == 0 && j == 0) atomicAdd(&p.ws->rows_started, 1u);
     }
     flush_stats(p, my_iters, my_pix);
-    if (threadIdx.y == 0) cta_clock_end(p, clk);
+    MANDEL_CTA_CLOCK_END();
 }
 
 #undef MANDEL_STEP

@@ -658,3 +658,57 @@ def test_enqueued_renders_on_two_streams(mandel, oracle):
     torch.cuda.synchronize()
     _assert_same(_host(oa), wa, "rank stream 1")
     _assert_same(_host(ob), wb, "rank stream 2")
+
+
+STAGE_CASES = [
+    # (label, config, options, expected store mode)
+    ("aligned", wl.C1.with_(W=640, H=480, iter_max=3000), {"stage": 1}, "staged_vec"),
+    ("W%4", wl.C1.with_(W=641, H=233, iter_max=3000), {"stage": 1}, "staged"),
+    ("tile_rows1", wl.C1.with_(W=512, H=97, iter_max=2000), {"stage": 1, "tile_rows": 1}, "staged_vec"),
+    ("tiny_tiles", wl.C1.with_(W=96, H=77, iter_max=2000), {"stage": 1, "tile_px": 1, "tile_rows": 1}, "staged"),
+    ("tile_px7", wl.C1.with_(W=203, H=64, iter_max=900), {"stage": 1, "tile_px": 7}, "staged"),
+    ("direct", wl.C1.with_(W=640, H=480, iter_max=3000), {"stage": -1}, "direct"),
+    # default: the map is this GPU's own HBM (logical ranks share the device) -> direct
+    ("auto_local", wl.C1.with_(W=640, H=480, iter_max=3000), {}, "direct"),
+    # interior-heavy: slow interior pixels hold their 8x8 blocks while the stream moves on,
+    # so ring entries are evicted (partial blocks stored, the rest stored directly)
+    ("evict", wl.Config("evict", -0.9, 0.3, -0.6, 0.6, 512, 384, 20000, 2.0, "fp64"), {"stage": 1}, "staged_vec"),
+    ("evict_f32", wl.Config("evict", -0.9, 0.3, -0.6, 0.6, 512, 384, 20000, 2.0, "fp32"), {"stage": 1},
+     "staged_vec"),
+]
+
+
+@pytest.mark.parametrize("kernel", ["refill", "batch8x2", "batch8x1", "batch8x4", "lazy2", "lazy1"])
+@pytest.mark.parametrize("case", STAGE_CASES, ids=[c[0] for c in STAGE_CASES])
+def test_store_staging(mandel, oracle, case, kernel):
+    """Coalesced, vectorised stores (north_star): counts are staged per
+    8x8 block in shared memory and whole blocks stored as 32-B rows with 16-B stores;
+    misaligned maps and narrow blocks store count by count, evicted blocks partly
+    directly.  Every mode gives the oracle's map, for every scheme and a misaligned
+    destination."""
+    torch = _torch()
+    label, cfg, opts, mode = case
+    want = oracle.render(cfg)
+    for scheme, n in (("block", 1), ("fcfs", 1), ("cyclic", 3), ("fcfs", 4)):
+        out, st = _render_dev(mandel, cfg, scheme, n, kernel=kernel, **opts)
+        _assert_same(_host(out), want, f"{label}/{kernel}/{scheme}/N={n}")
+        assert st["store_mode"] == mode, (label, st["store_mode"])
+    # a destination 4 bytes past a 16-B boundary: staged, but no vector stores
+    buf = torch.zeros(cfg.pixels + 4, dtype=torch.int32, device="cuda:0")
+    st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, "fcfs", 1, out_dev0=buf.data_ptr() + 4,
+                                 kernel=kernel, **opts)
+    got = buf[1:1 + cfg.pixels].reshape(cfg.H, cfg.W)
+    _assert_same(_host(got), want, f"{label}/{kernel}/misaligned")
+    assert int(buf[0]) == 0 and int(buf[1 + cfg.pixels]) == 0  # nothing outside the map
+    assert st["store_mode"] == ("direct" if mode == "direct" else "staged")
+
+
+def test_store_staging_variants_without_instantiation(mandel, oracle):
+    """stage = 1 on a kernel with no staged instantiation (per-update EAGER, check every 4,
+    ADAPTIVE, static) stores directly and says so."""
+    cfg = wl.C1.with_(W=320, H=200, iter_max=1500)
+    want = oracle.render(cfg)
+    for kernel in ("refill1", "batch4x2", "adaptive2", "static"):
+        out, st = _render_dev(mandel, cfg, "block", 2, kernel=kernel, stage=1)
+        _assert_same(_host(out), want, kernel)
+        assert st["store_mode"] == "direct", (kernel, st["store_mode"])
