@@ -193,6 +193,8 @@ typedef struct mandel_options {
                                 count); -1 -> every count stored directly (4-B stores);
                                 0 -> default: staged when the map is on another GPU (the fused
                                 gather's NVLink peer stores), direct into the rank's own HBM    */
+    int      ctas_per_sm;    /* persistent kernels: at most this many resident CTAs per SM (grid =
+                                min(this, occupancy) x SMs); 0 -> the occupancy maximum            */
 } mandel_options;
 
 /*

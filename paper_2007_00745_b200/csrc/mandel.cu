@@ -162,6 +162,8 @@ struct DeviceCtx {
     bool peer_to0 = false;
     uint32_t* scratch = nullptr;  // the view probe's compact sample band (every 16th row)
     size_t scratch_bytes = 0;
+    void* pstate = nullptr;       // the view probe's own work state
+    size_t pstate_bytes = 0;
 };
 
 struct RankCtx {
@@ -172,8 +174,13 @@ struct RankCtx {
     // the state waits on it, so enqueue-only renders on different streams never share it
     // mid-flight (the caller may pass a different stream per call)
     cudaEvent_t used = nullptr;
-    void* state = nullptr;  // WorkState + chunk_map
+    // two halves of state_bytes each (WorkState + chunk_map): render n uses half par, and its
+    // kernel zeroes the other half for render n + 1 -- no host memset between renders
+    void* state = nullptr;
     size_t state_bytes = 0;
+    int par = 0;
+    size_t zeroed[2] = {0, 0};  // bytes of each half known to be zero
+    void* half(int k) const { return static_cast<char*>(state) + (size_t)k * state_bytes; }
 };
 
 constexpr int kMaxBands = 32;
@@ -181,7 +188,9 @@ constexpr int kMaxBands = 32;
 struct Root {
     uint32_t* image = nullptr;  // library-owned map on device 0
     size_t image_bytes = 0;
-    uint32_t* fcfs_ctr = nullptr;
+    uint32_t* fcfs_ctr = nullptr;  // two counter words (0 and 32): render n claims from word
+    int ctr_par = 0;               // ctr_par, its rank-0 kernel zeroes the other for render n+1
+    bool ctr_zeroed[2] = {false, false};
     cudaEvent_t start = nullptr, done = nullptr, d2h = nullptr;
     // pipelined one-GPU hand-off: band states, a second compute stream, a copy stream
     void* band_state = nullptr;
@@ -324,15 +333,18 @@ struct KernelChoice {
     int variant, ilp, minb;
     int bt;          // EAGER: z-updates per escape check (1 = every update; 4, 8, 16 = batched, R18)
     int packed = 0;  // fp32 batched loop on FADD2/FMUL2 slot pairs (set by build_params)
+    int ctas = 0;    // resident CTAs per SM cap (0: the occupancy maximum)
 };
 // ILP2 runs with ptxas' unconstrained schedule (74 registers, 3 CTAs of 256 threads per SM).
 // Batched escape check with a whole-batch replay on a hit (R18), measured per config
 // (profiles/r01_sweep_batch.jsonl, Giter/s): fp64 C2 check-every-8 ILP2 2061 (per-update
 // check 1722), C5 2360 (1962); fp32 C3 check-every-8 ILP1 3346 (per-update ILP4 2504).
 // fp32 stops at 8 updates per test: R18's drift bound covers no more (16 measured 3438).
-constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 3, 8},    // fp64
-                                            {MANDEL_KERNEL_EAGER, 1, 3, 8},    // fp32
-                                            {MANDEL_KERNEL_EAGER, 2, 3, 8}};   // fp64 FMA
+// fp32 ILP1 fits 5 CTAs of 256 threads per SM (48 registers); 4 resident CTAs run C3 at
+// 3584 Giter/s against 3491 with 5 (profiles/r02m_sweep.jsonl), so the default caps it.
+constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 3, 8, 0, 0},    // fp64
+                                            {MANDEL_KERNEL_EAGER, 1, 3, 8, 0, 4},    // fp32
+                                            {MANDEL_KERNEL_EAGER, 2, 3, 8, 0, 0}};   // fp64 FMA
 constexpr uint32_t kDefaultRefillLanes = 16;  // LAZY on C4: 8 -> 1509, 16 -> 1555 Giter/s
 constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
 constexpr double kDefaultBandTaper = 0.7;  // band pair p holds a 0.7^p share of the rows
@@ -401,8 +413,11 @@ int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
         if (rc.state) CK(cudaFree(rc.state));
         rc.state = nullptr;
         rc.state_bytes = 0;
-        CK(cudaMalloc(&rc.state, state_bytes));
+        CK(cudaMalloc(&rc.state, 2 * state_bytes));
+        CK(cudaMemset(rc.state, 0, 2 * state_bytes));
         rc.state_bytes = state_bytes;
+        rc.par = 0;
+        rc.zeroed[0] = rc.zeroed[1] = state_bytes;
     }
     (void)user_stream;
     return MANDEL_OK;
@@ -605,6 +620,9 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
             ls.smem = (size_t)smem_sm / 2 + 1024;
             ls.grid = dim3((unsigned)std::min(o->max_sms, dc.sms));
         } else {
+            if (o && o->ctas_per_sm < 0) return fail(MANDEL_EINVAL, "options.ctas_per_sm must be >= 0");
+            const int cap = (o && o->ctas_per_sm > 0) ? o->ctas_per_sm : kc.ctas;
+            if (cap > 0 && cap < occ) occ = cap;
             ls.grid = dim3((unsigned)(occ * dc.sms));
         }
     } else {
@@ -708,8 +726,8 @@ constexpr uint32_t kProbeStride = 16;
 // on the probing device (band mode: band row = sample index), never into the caller's
 // map -- under mandel_render_rank that map is rank 0's shared image on another GPU.
 int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, uint32_t iter_max,
-                int dtype, const mandel_options* o, void* state, size_t state_cap,
-                int device, cudaStream_t s, KernelChoice& out) {
+                int dtype, const mandel_options* o, size_t state_cap, int device, cudaStream_t s,
+                KernelChoice& out) {
     const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
     out = kDefaultChoice[fi];
     if (o && (o->kernel != MANDEL_KERNEL_REFILL || o->ilp || o->min_ctas > 1)) return MANDEL_OK;
@@ -735,6 +753,17 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
         CK(cudaMalloc(&dc.scratch, sbytes));
         dc.scratch_bytes = sbytes;
     }
+    if (dc.pstate_bytes < state_cap) {  // the probe's own work state (the ranks' halves are theirs)
+        if (dc.pstate) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaFree(dc.pstate));
+        }
+        dc.pstate = nullptr;
+        dc.pstate_bytes = 0;
+        CK(cudaMalloc(&dc.pstate, state_cap));
+        dc.pstate_bytes = state_cap;
+    }
+    void* const pst = dc.pstate;
     const KernelChoice cand[2] = {{kVariantProbe, kDefaultChoice[fi].ilp, kDefaultChoice[fi].minb, 1},
                                   {MANDEL_KERNEL_LAZY, 2, 1, 1}};
     mandel_options po{};
@@ -752,18 +781,16 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     LaunchSpec ls;
-    int rc = build_params(d, W, H, iter_max, dtype, MANDEL_BLOCK, 1, 0, &po, dc.scratch, state, state_cap,
+    int rc = build_params(d, W, H, iter_max, dtype, MANDEL_BLOCK, 1, 0, &po, dc.scratch, pst, state_cap,
                           nullptr, false, device, ls, &pl, &cand[0]);
     if (rc) { cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
-    CK(cudaStreamWaitEvent(s, g_rank[0].used, 0));  // an enqueued render may still use the state
-    CK(cudaMemsetAsync(state, 0, state_cap, s));
+    CK(cudaMemsetAsync(pst, 0, state_cap, s));
     CK(cudaEventRecord(e0, s));
     rc = launch(ls, s);
     if (rc) { cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
     CK(cudaEventRecord(e1, s));
-    CK(cudaEventRecord(g_rank[0].used, s));
     mandel::WorkState ws;
-    CK(cudaMemcpyAsync(&ws, state, sizeof(ws), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ws, pst, sizeof(ws), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -991,7 +1018,11 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         CK(cudaEventCreate(&g_root.done));
         CK(cudaEventCreate(&g_root.d2h));
     }
-    if (!g_root.fcfs_ctr) CK(cudaMalloc(&g_root.fcfs_ctr, 256));
+    if (!g_root.fcfs_ctr) {
+        CK(cudaMalloc(&g_root.fcfs_ctr, 256));
+        CK(cudaMemset(g_root.fcfs_ctr, 0, 256));
+        g_root.ctr_zeroed[0] = g_root.ctr_zeroed[1] = true;
+    }
     uint32_t* image = out_dev0;
     if (!image) {
         if (g_root.image_bytes < bytes) {
@@ -1011,8 +1042,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         rc = ensure_rank(0, 0, sbytes, nullptr);
         if (rc) return rc;
         cudaStream_t sp = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
-        rc = auto_choice(d, bounds, W, H, iter_max, dtype, opts, g_rank[0].state,
-                         g_rank[0].state_bytes, 0, sp, kc);
+        rc = auto_choice(d, bounds, W, H, iter_max, dtype, opts, sbytes, 0, sp, kc);
         if (rc) return rc;
     }
     const bool auto_k = !opts || opts->kernel == MANDEL_KERNEL_REFILL;
@@ -1050,45 +1080,60 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         return rc;
     }
     std::vector<LaunchSpec> specs(ngpus);
+    const int cp = g_root.ctr_par;  // the counter word this render claims from
     for (int r = 0; r < ngpus; ++r) {
         const int dev = r % ndev;
         rc = ensure_rank(r, dev, sbytes, nullptr);
         if (rc) return rc;
-        rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, g_rank[r].state,
-                          g_rank[r].state_bytes, g_root.fcfs_ctr, nphys > 1, dev, specs[r], nullptr, kcp,
+        RankCtx& rk = g_rank[r];
+        rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, rk.half(rk.par),
+                          rk.state_bytes, g_root.fcfs_ctr + 32 * cp, nphys > 1, dev, specs[r], nullptr, kcp,
                           dev != 0);
         if (rc) return rc;
+        // the kernel zeroes the rank's other half (and rank 0 the other counter word) for the
+        // next render
+        specs[r].p.zero_next = static_cast<uint32_t*>(rk.half(rk.par ^ 1));
+        specs[r].p.zero_words = (uint32_t)(sbytes / sizeof(uint32_t));
+        specs[r].p.zero_ctr = r == 0 ? g_root.fcfs_ctr + 32 * (cp ^ 1) : nullptr;
     }
     cudaStream_t s0 = stream0v ? (cudaStream_t)stream0v : g_rank[0].stream;
-    // rank 0 orders everything: reset state, start event, then every rank waits on it
+    // events: only when the call times or waits (statistics, host output) or orders ranks
+    const bool timed = stats || out_host || ngpus > 1;
+    // rank 0 orders everything: start event, then every rank waits on it
     CK(cudaSetDevice(0));
-    // the counter and the rank states are library-owned and reused: an earlier enqueued
-    // render (possibly on another stream) must be done with them before they are reset
+    // the counter words and the rank states are library-owned and reused: an earlier
+    // enqueued render (possibly on another stream) must be done with them first
     for (int r = 0; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].used, 0));
-    CK(cudaMemsetAsync(g_root.fcfs_ctr, 0, 256, s0));
-    CK(cudaMemsetAsync(g_rank[0].state, 0, sbytes, s0));
-    CK(cudaEventRecord(g_root.start, s0));
+    if (!g_root.ctr_zeroed[cp]) CK(cudaMemsetAsync(g_root.fcfs_ctr + 32 * cp, 0, sizeof(uint32_t), s0));
+    if (g_rank[0].zeroed[g_rank[0].par] < sbytes) CK(cudaMemsetAsync(g_rank[0].half(g_rank[0].par), 0, sbytes, s0));
+    if (timed) CK(cudaEventRecord(g_root.start, s0));
     for (int r = 1; r < ngpus; ++r) {
         RankCtx& rk = g_rank[r];
         CK(cudaSetDevice(rk.device));
         CK(cudaStreamWaitEvent(rk.stream, g_root.start, 0));
-        CK(cudaMemsetAsync(rk.state, 0, sbytes, rk.stream));
+        if (rk.zeroed[rk.par] < sbytes) CK(cudaMemsetAsync(rk.half(rk.par), 0, sbytes, rk.stream));
     }
     int launches = 0;
     for (int r = 0; r < ngpus; ++r) {
         RankCtx& rk = g_rank[r];
         cudaStream_t s = r == 0 ? s0 : rk.stream;
         CK(cudaSetDevice(rk.device));
-        CK(cudaEventRecord(rk.k0, s));
+        if (timed) CK(cudaEventRecord(rk.k0, s));
         rc = launch(specs[r], s);
         if (rc) return rc;
         ++launches;
-        CK(cudaEventRecord(rk.k1, s));
+        if (timed) CK(cudaEventRecord(rk.k1, s));
+        rk.zeroed[rk.par] = 0;
+        rk.zeroed[rk.par ^ 1] = sbytes;
+        rk.par ^= 1;
     }
+    g_root.ctr_zeroed[cp] = false;
+    g_root.ctr_zeroed[cp ^ 1] = true;
+    g_root.ctr_par = cp ^ 1;
     CK(cudaSetDevice(0));
     for (int r = 1; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].k1, 0));
-    CK(cudaEventRecord(g_root.done, s0));
-    // every rank's state and the shared counter are free once GPU 0's stream passes here
+    if (timed) CK(cudaEventRecord(g_root.done, s0));
+    // every rank's state and the counter are free once GPU 0's stream passes here
     for (int r = 0; r < ngpus; ++r) {
         CK(cudaSetDevice(g_rank[r].device));
         CK(cudaEventRecord(g_rank[r].used, r == 0 ? s0 : g_rank[r].stream));
@@ -1105,7 +1150,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     for (int r = 0; r < ngpus; ++r) {
         RankCtx& rk = g_rank[r];
         CK(cudaSetDevice(rk.device));
-        CK(cudaMemcpyAsync(&ws[r], rk.state, sizeof(mandel::WorkState), cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(&ws[r], specs[r].p.ws, sizeof(mandel::WorkState), cudaMemcpyDeviceToHost,
                            r == 0 ? s0 : rk.stream));
     }
     for (int r = 0; r < ngpus; ++r) {
@@ -1279,7 +1324,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
                         !(scheme == MANDEL_FCFS_MASTER && rank == 0);  // the master computes nothing
     if (auto_k) {
         const double bounds[5] = {xmin, xmax, ymin, ymax, R};
-        rc = auto_choice(d, bounds, W, H, iterMax, dtype, opts, rk.state, rk.state_bytes, dev, s, kc);
+        rc = auto_choice(d, bounds, W, H, iterMax, dtype, opts, sbytes, dev, s, kc);
         if (rc) return rc;
     }
     LaunchSpec ls;
@@ -1287,21 +1332,27 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
     // the fused gather: a rank other than 0 stores into rank 0's map on another GPU (its
     // band, with options.band_out, is local)
     const bool remote = rank != 0 && !(opts && opts->band_out) && !same_device(out_root, dev);
-    rc = build_params(d, W, H, iterMax, dtype, scheme, nranks, rank, opts, out_root, rk.state,
+    void* const cur = rk.half(rk.par);
+    rc = build_params(d, W, H, iterMax, dtype, scheme, nranks, rank, opts, out_root, cur,
                       rk.state_bytes, fcfs_counter, nranks > 1, dev, ls, nullptr, auto_k ? &kc : nullptr, remote);
     if (rc) return rc;
+    ls.p.zero_next = static_cast<uint32_t*>(rk.half(rk.par ^ 1));  // the next render's state half
+    ls.p.zero_words = (uint32_t)(sbytes / sizeof(uint32_t));
     const double t0 = now_ms();
     CK(cudaStreamWaitEvent(s, rk.used, 0));  // an earlier enqueued render may still use the state
-    CK(cudaMemsetAsync(rk.state, 0, sbytes, s));
-    CK(cudaEventRecord(rk.k0, s));
+    if (rk.zeroed[rk.par] < sbytes) CK(cudaMemsetAsync(cur, 0, sbytes, s));
+    const bool band = opts && opts->band_out;
+    if (stats || band) CK(cudaEventRecord(rk.k0, s));
     rc = launch(ls, s);
     if (rc) return rc;
-    CK(cudaEventRecord(rk.k1, s));
+    if (stats || band) CK(cudaEventRecord(rk.k1, s));
     CK(cudaEventRecord(rk.used, s));
-    const bool band = opts && opts->band_out;
+    rk.zeroed[rk.par] = 0;
+    rk.zeroed[rk.par ^ 1] = sbytes;
+    rk.par ^= 1;
     if (!stats && !band) return MANDEL_OK;  // asynchronous: enqueued on the stream, not awaited
     mandel::WorkState ws;
-    CK(cudaMemcpyAsync(&ws, rk.state, sizeof(ws), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ws, cur, sizeof(ws), cudaMemcpyDeviceToHost, s));
     std::vector<uint32_t> cmap;
     if (band && ls.p.scheme == MANDEL_FCFS) {
         cmap.resize((size_t)ls.p.nchunks + 1);
@@ -1562,11 +1613,13 @@ void mandel_shutdown(void) {
         }
     }
     for (size_t dv = 0; dv < g_dev.size(); ++dv) {
-        if (!g_dev[dv].scratch) continue;
         cudaSetDevice((int)dv);
-        cudaFree(g_dev[dv].scratch);
+        if (g_dev[dv].scratch) cudaFree(g_dev[dv].scratch);
+        if (g_dev[dv].pstate) cudaFree(g_dev[dv].pstate);
         g_dev[dv].scratch = nullptr;
         g_dev[dv].scratch_bytes = 0;
+        g_dev[dv].pstate = nullptr;
+        g_dev[dv].pstate_bytes = 0;
     }
     g_root = Root();
     g_auto.clear();

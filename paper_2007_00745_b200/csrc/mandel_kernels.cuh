@@ -119,6 +119,11 @@ struct Params {
     WorkState* ws;                   // this rank's state (local memory)
     uint32_t* chunk_map;             // this rank's local->global chunk table (local memory)
     uint32_t* fcfs_ctr;              // shared global chunk counter (GPU 0's memory)
+    // the next render's work state (the other half of the rank's state) and counter word:
+    // zeroed by this launch's first CTA, so renders need no host memset between them
+    uint32_t* zero_next;
+    uint32_t zero_words;
+    uint32_t* zero_ctr;
 };
 
 // Arithmetic policies: the storage type T, its RN operations, the escape-test bit
@@ -344,14 +349,19 @@ __device__ __forceinline__ uint32_t claim_chunk(const Params& p) {
     return kChunkDone;
 }
 
+// Wait until local chunk k is bound (warp-collective: lane 0 reads, every lane loops on
+// the broadcast value, so no lane spins alone while the others wait at a warp barrier).
 __device__ __forceinline__ uint32_t wait_bound(const Params& p, uint32_t k) {
-    uint32_t g;
+    const unsigned FULL = 0xffffffffu;
     unsigned ns = 32;
-    while ((g = ld_volatile(&p.chunk_map[k])) == 0) {
+    for (;;) {
+        uint32_t g = 0;
+        if ((threadIdx.x & 31) == 0) g = ld_volatile(&p.chunk_map[k]);
+        g = __shfl_sync(FULL, g, 0);
+        if (g != 0) return g;
         __nanosleep(ns);
         ns = min(ns * 2, 256u);
     }
-    return g;
 }
 
 // A tile: `nrows` row slots x `cols` columns starting at column j0.  `base` is the
@@ -364,12 +374,6 @@ struct Tile {
     uint32_t base, nrows, j0, cols;
     uint32_t slot;  // the rank's local slot of the first row (its band row in band mode)
 };
-
-__device__ __forceinline__ Tile bcast_tile(const Tile& t) {
-    const unsigned FULL = 0xffffffffu;
-    return Tile{__shfl_sync(FULL, t.base, 0), __shfl_sync(FULL, t.nrows, 0), __shfl_sync(FULL, t.j0, 0),
-                __shfl_sync(FULL, t.cols, 0), __shfl_sync(FULL, t.slot, 0)};
-}
 
 // Pixel q of tile t -> image (row, col) and the row of the output buffer it is stored
 // to: the image row, or (band mode) the rank-local band row = its local slot.
@@ -526,19 +530,36 @@ __device__ __forceinline__ void stage_drain(const Params& p, StageEntry* ring, u
 
 // (ck, cg) caches lane 0's last local->global chunk binding, so only the first
 // draw in each chunk reads chunk_map (an L2 round trip) -- init ck = 0xffffffff.
-__device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck, uint32_t& cg) {
-    const uint32_t t = atomicAdd(&p.ws->tile_ctr, 1u);
+// tn: each warp's first tile is its own index in the grid -- no atomic, so the launch
+// does not start with every warp of the rank hitting the one counter at once; later
+// draws take counter values from the warp count on (init tn = first_tile(), then
+// kTileFirstDone).  (Requesting the next index one tile ahead was tried: the tiles
+// reserved by busy warps lengthened the tail, C2 -3%.)
+constexpr uint32_t kTileFirstDone = 0xffffffffu;
+__device__ __forceinline__ uint32_t first_tile() { return blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); }
+__device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck, uint32_t& cg, uint32_t& tn) {
+    // warp-collective: lane 0 issues the atomics, every lane computes the (uniform) tile
+    const unsigned FULL = 0xffffffffu;
+    const bool l0 = (threadIdx.x & 31) == 0;
+    uint32_t t = 0;
+    if (tn != kTileFirstDone) {
+        t = tn;  // the warp's first tile
+        tn = kTileFirstDone;
+    } else {
+        if (l0) t = atomicAdd(&p.ws->tile_ctr, 1u) + gridDim.x * kWarpsPerCta;
+        t = __shfl_sync(FULL, t, 0);
+    }
     const uint32_t grp = t / p.tiles_per_row;
     const uint32_t seg = t - grp * p.tiles_per_row;
     const uint32_t slot = grp * p.tile_rows;
-    tl.j0 = seg * p.tile_w;
-    tl.cols = min(p.tile_w, p.W - tl.j0);
     if (p.scheme != kSchemeFcfs) {
         if (slot >= p.nslots) return kTileNone;
+        tl.j0 = seg * p.tile_w;
+        tl.cols = min(p.tile_w, p.W - tl.j0);
         tl.base = slot;
         tl.slot = slot;
         tl.nrows = min(p.tile_rows, p.nslots - slot);
-        if (seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
+        if (l0 && seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
         return kTileOk;
     }
     const uint32_t k = slot / p.chunk_rows;
@@ -552,13 +573,13 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
             // first tile of local chunk k: bind chunk 0 if k == 0, then bind chunk k+1 one
             // chunk ahead (claims stay in local-chunk order; chunk k is already bound when
             // its first tile is drawn, so warps rarely wait on a claim in flight)
-            if (k == 0) {
+            if (k == 0 && l0) {
                 const uint32_t g0 = claim_chunk(p);
                 fcfs_delay(2);
                 st_volatile(&p.chunk_map[0], g0);
             }
             g = wait_bound(p, k);
-            if (k + 1 <= p.nchunks) {
+            if (k + 1 <= p.nchunks && l0) {
                 const uint32_t gn = g == kChunkDone ? kChunkDone : claim_chunk(p);
                 fcfs_delay(3);  // the claim is made, its binding not yet visible
                 st_volatile(&p.chunk_map[k + 1], gn);
@@ -572,10 +593,12 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
     if (g == kChunkDone) return kTileNone;
     const uint32_t row = (g - 1) * p.chunk_rows + r;
     if (row >= p.H) return kTileSkip;
+    tl.j0 = seg * p.tile_w;
+    tl.cols = min(p.tile_w, p.W - tl.j0);
     tl.base = row;
     tl.slot = slot;
     tl.nrows = min(p.tile_rows, p.H - row);
-    if (seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
+    if (l0 && seg == 0) atomicAdd(&p.ws->rows_started, tl.nrows);
     return kTileOk;
 }
 
@@ -605,6 +628,15 @@ __device__ __forceinline__ void cta_clock_end(const Params& p, const unsigned lo
     __shared__ unsigned long long mandel_clk_sm_[2];   \
     cta_clock_start(mandel_clk_sm_)
 #define MANDEL_CTA_CLOCK_END() cta_clock_end(p, mandel_clk_sm_)
+
+// The first CTA zeroes the next render's state half and counter word (Params::zero_next).
+__device__ __forceinline__ void zero_next_state(const Params& p) {
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+        const uint32_t tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
+        for (uint32_t i = tid; i < p.zero_words; i += nt) p.zero_next[i] = 0u;
+        if (tid == 0 && p.zero_ctr) *p.zero_ctr = 0u;
+    }
+}
 
 __device__ __forceinline__ void flush_loop_stats(const Params& p, uint32_t witers, uint32_t exits) {
     if ((threadIdx.x & 31) == 0 && exits) {
@@ -814,6 +846,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     MANDEL_CTA_CLOCK_START();
+    zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
     const unsigned FULL = 0xffffffffu;
@@ -848,7 +881,8 @@ escape_refill_kernel(const Params p) {
     Tile tl = {0u, 0u, 0u, 0u, 0u};
     uint32_t tq = 0, tqend = 0;
     bool more = true;
-    uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
+    uint32_t ck_ = 0xffffffffu, cg_ = 0;  // the warp's chunk-binding cache (draw_tile)
+    uint32_t tn_ = first_tile();          // the warp's first tile (draw_tile)
     fcfs_delay(4);
     unsigned need[ILP];
 #pragma unroll
@@ -869,12 +903,9 @@ escape_refill_kernel(const Params p) {
             for (;;) {
                 if (tq >= tqend) {
                     if (!more) break;
-                    int st = 0;
-                    if (lane == 0) st = draw_tile(p, tl, ck_, cg_);
-                    st = __shfl_sync(FULL, st, 0);
+                    const int st = draw_tile(p, tl, ck_, cg_, tn_);  // warp-uniform
                     if (st == kTileNone) { more = false; break; }
                     if (st == kTileSkip) continue;
-                    tl = bcast_tile(tl);
                     tq = 0;
                     tqend = tl.nrows * tl.cols;
                     tile_e0 = (tile_e0 + sub_open) & (kStageEntries - 1);
@@ -1014,6 +1045,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_lazy_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     MANDEL_CTA_CLOCK_START();
+    zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -1049,7 +1081,8 @@ escape_lazy_kernel(const Params p) {
     Tile tl = {0u, 0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
     uint32_t tq = 0, tqend = 0;
     bool more = true;
-    uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
+    uint32_t ck_ = 0xffffffffu, cg_ = 0;  // the warp's chunk-binding cache (draw_tile)
+    uint32_t tn_ = first_tile();          // the warp's first tile (draw_tile)
 #if MANDEL_LAZY_PROF
     unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -1070,12 +1103,9 @@ escape_lazy_kernel(const Params p) {
         while (served < nd) {
             if (tq >= tqend) {
                 if (!more) break;
-                int st = 0;
-                if (lane == 0) st = draw_tile(p, tl, ck_, cg_);
-                st = __shfl_sync(FULL, st, 0);
+                const int st = draw_tile(p, tl, ck_, cg_, tn_);  // warp-uniform
                 if (st == kTileNone) { more = false; break; }
                 if (st == kTileSkip) continue;
-                tl = bcast_tile(tl);
                 tq = 0;
                 tqend = tl.nrows * tl.cols;
                 tile_e0 = (tile_e0 + sub_open) & (kStageEntries - 1);
@@ -1207,6 +1237,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_adaptive_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     MANDEL_CTA_CLOCK_START();
+    zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;
@@ -1231,7 +1262,8 @@ escape_adaptive_kernel(const Params p) {
     Tile tl = {0u, 0u, 0u, 0u, 0u};  // warp-uniform tile cursor (as escape_refill_kernel)
     uint32_t tq = 0, tqend = 0;
     bool more = true;
-    uint32_t ck_ = 0xffffffffu, cg_ = 0;  // lane 0's chunk-binding cache (draw_tile)
+    uint32_t ck_ = 0xffffffffu, cg_ = 0;  // the warp's chunk-binding cache (draw_tile)
+    uint32_t tn_ = first_tile();          // the warp's first tile (draw_tile)
     bool lazy = false;           // warp-uniform run mode
     uint32_t ema = 4 * p.adapt_lo + 64;  // EMA of eager run lengths (x4, fixed point)
     uint32_t lazy_left = 0;      // lazy runs left before the next eager probe
@@ -1252,12 +1284,9 @@ escape_adaptive_kernel(const Params p) {
             for (;;) {
                 if (tq >= tqend) {
                     if (!more) break;
-                    int st = 0;
-                    if (lane == 0) st = draw_tile(p, tl, ck_, cg_);
-                    st = __shfl_sync(FULL, st, 0);
+                    const int st = draw_tile(p, tl, ck_, cg_, tn_);  // warp-uniform
                     if (st == kTileNone) { more = false; break; }
                     if (st == kTileSkip) continue;
-                    tl = bcast_tile(tl);
                     tq = 0;
                     tqend = tl.nrows * tl.cols;
                 }
@@ -1370,6 +1399,7 @@ template <typename AR>
 __global__ void __launch_bounds__(kCtaThreads)
 escape_static_kernel(const Params p) {
     MANDEL_CTA_CLOCK_START();
+    zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
     typedef typename A::bits_t B;

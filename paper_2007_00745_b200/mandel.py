@@ -125,6 +125,7 @@ class mandel_options(ctypes.Structure):
         ("async_host", ctypes.c_int),
         ("check_every", ctypes.c_int),
         ("stage", ctypes.c_int),
+        ("ctas_per_sm", ctypes.c_int),
     ]
 
 
@@ -251,7 +252,7 @@ def _buf(a, nbytes: int, name: str) -> int | None:
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
           tile_rows=0, no_pack=False, band_out=False, band_taper=0, max_sms=0, async_host=False,
-          stage=0):
+          stage=0, ctas_per_sm=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -272,6 +273,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.max_sms = max_sms or 0
     o.async_host = 1 if async_host else 0
     o.stage = int(stage)
+    o.ctas_per_sm = int(ctas_per_sm)
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -303,7 +305,7 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
                      bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0,
-                     max_sms=0, async_host=False, stage=0, want_stats=True):
+                     max_sms=0, async_host=False, stage=0, ctas_per_sm=0, want_stats=True):
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict; want_stats=False (device output only)
@@ -315,7 +317,7 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
               refill_lanes=refill_lanes, ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo,
               adapt_hi=adapt_hi, bands=bands, check_every=check_every, tile_rows=tile_rows,
               no_pack=no_pack, band_taper=band_taper, max_sms=max_sms, async_host=async_host,
-              stage=stage)
+              stage=stage, ctas_per_sm=ctas_per_sm)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), host_p,
                                 dev_p, stream0, ctypes.byref(st) if st is not None else None)

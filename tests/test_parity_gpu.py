@@ -712,3 +712,34 @@ def test_store_staging_variants_without_instantiation(mandel, oracle):
         out, st = _render_dev(mandel, cfg, "block", 2, kernel=kernel, stage=1)
         _assert_same(_host(out), want, kernel)
         assert st["store_mode"] == "direct", (kernel, st["store_mode"])
+
+
+def test_back_to_back_renders_reset_state_in_kernel(mandel, oracle):
+    """Consecutive renders need no host memset: each launch's first CTA zeroes the other
+    half of the rank's work state and the other FCFS counter word for the next render.
+    Enqueued renders of different sizes (a larger chunk map falls back to a host memset),
+    schemes, rank counts and streams, then every map and a final statistics call checked."""
+    torch = _torch()
+    views = [wl.C1.with_(W=257, H=37, iter_max=700), wl.C1.with_(W=300, H=777, iter_max=400),
+             wl.C1.with_(W=96, H=1500, iter_max=300), wl.C1.with_(W=257, H=37, iter_max=700)]
+    want = [oracle.render(v) for v in views]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs, plan = [], []
+    for rep in range(3):
+        for k, v in enumerate(views):
+            scheme, n = [("fcfs", 1), ("block", 1), ("fcfs", 3), ("cyclic", 2)][(k + rep) % 4]
+            o = torch.zeros((v.H, v.W), dtype=torch.int32, device="cuda:0")
+            torch.cuda.synchronize()
+            st = [s1, s2][(k + rep) % 2].cuda_stream
+            mandel.mandel_render_ex(*v.args(), "fp64", scheme, n, out_dev0=o, stream0=st, logical_ranks=n > 1,
+                                    want_stats=False, kernel=["refill", "lazy2"][rep % 2])
+            outs.append(o)
+            plan.append(k)
+    torch.cuda.synchronize()
+    for o, k in zip(outs, plan):
+        _assert_same(_host(o), want[k], f"view {k}")
+    for v, w in zip(views, want):
+        for scheme, n in (("fcfs", 1), ("fcfs", 3)):
+            out, st = _render_dev(mandel, v, scheme, n)
+            _assert_same(_host(out), w, f"stats {scheme}/{n}")
+            assert st["chunks_claimed"] == -(-v.H // 16) and st["pixels"] == v.pixels
