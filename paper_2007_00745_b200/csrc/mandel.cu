@@ -527,6 +527,8 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     p.nslots = pl.nslots; p.base0 = pl.base0; p.stride0 = pl.stride0; p.count0 = pl.count0; p.base1 = pl.base1;
     p.chunk_rows = chunk;
     p.nchunks = (uint32_t)(((uint64_t)H + chunk - 1) / chunk);
+    // one claimant (N = 1, not the paper's master/worker) claims 16 chunks at a time
+    p.claim_batch = (nranks == 1 && scheme == MANDEL_FCFS) ? 16u : 1u;
     if (kscheme == MANDEL_FCFS) {
         uint64_t tiles = (uint64_t)(p.nchunks + 1) * (chunk / trows) * p.tiles_per_row;
         if (tiles >= 0xF0000000ull) return fail(MANDEL_EINVAL, "FCFS tile space exceeds 32 bits; raise tile_px");
@@ -731,7 +733,9 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
     const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
     out = kDefaultChoice[fi];
     if (o && (o->kernel != MANDEL_KERNEL_REFILL || o->ilp || o->min_ctas > 1)) return MANDEL_OK;
-    if (H < 32 * kProbeStride || (uint64_t)W * H < (1u << 20)) return MANDEL_OK;  // too small to matter
+    // too small to matter (below ~0.5 M pixels a render is a few tens of microseconds);
+    // C1 (800^2) is probed: LAZY's exact per-update record suits its short counts
+    if (H < 32 * kProbeStride || (uint64_t)W * H < (1u << 19)) return MANDEL_OK;
     ViewKey key{{bounds[0], bounds[1], bounds[2], bounds[3], bounds[4]}, W, H, iter_max, dtype};
     auto it = g_auto.find(key);
     if (it != g_auto.end()) {

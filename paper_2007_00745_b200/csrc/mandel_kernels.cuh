@@ -111,6 +111,7 @@ struct Params {
     // static schemes: slot s -> row s < count0 ? base0 + s*stride0 : base1 + (s - count0)
     uint32_t nslots, base0, stride0, count0, base1;
     uint32_t chunk_rows, nchunks;    // FCFS
+    uint32_t claim_batch;            // FCFS: chunks per claim (1 when ranks compete; more for one)
     uint32_t fcfs_sys;               // 1: the counter is shared across devices (system-scope atomics)
     uint32_t refill_lanes;           // lazy refill: leave the loop when this many lanes are free
     uint32_t adapt_lo, adapt_hi;     // adaptive: eager->lazy below adapt_lo iterations per run,
@@ -339,14 +340,27 @@ enum : int { kTileOk = 0, kTileSkip = 1, kTileNone = 2 };
 // an atomic on the shared counter in GPU 0's HBM -- system scope when ranks on other
 // GPUs claim from it too (NVLink), device scope otherwise.  Returns the chunk_map
 // entry: global chunk + 1, or kChunkDone once every chunk is taken.
-__device__ __forceinline__ uint32_t claim_chunk(const Params& p) {
-    fcfs_delay(1);
-    const uint32_t c = p.fcfs_sys ? atomicAdd_system(p.fcfs_ctr, 1u) : atomicAdd(p.fcfs_ctr, 1u);
-    if (c < p.nchunks) {
-        atomicAdd(&p.ws->chunks_claimed, 1u);
-        return c + 1;
+// Bind local chunks [k0, k0 + claim_batch) (up to nchunks) with one claim of that many
+// global chunks -- or to kChunkDone without a claim once the counter is known exhausted.
+// claim_batch is 1 whenever ranks compete for the counter (a claim reserves only the
+// next chunk, so the FCFS tail stays one chunk); a single claimant binds 16 at a time,
+// which shortens the chain of one-ahead bindings (each link an atomic round trip) that
+// bounds small views (C1: 50 chunks of cheap rows).  Called by one lane.
+__device__ __forceinline__ void bind_chunks(const Params& p, uint32_t k0, bool exhausted) {
+    const uint32_t nb = p.claim_batch;
+    uint32_t c = 0;
+    if (!exhausted) {
+        fcfs_delay(1);
+        c = p.fcfs_sys ? atomicAdd_system(p.fcfs_ctr, nb) : atomicAdd(p.fcfs_ctr, nb);
     }
-    return kChunkDone;
+    uint32_t got = 0;
+    for (uint32_t i = 0; i < nb && k0 + i <= p.nchunks; ++i) {
+        const bool ok = !exhausted && c + i < p.nchunks;
+        got += ok ? 1u : 0u;
+        if (i == 0) fcfs_delay(3);  // the claim is made, its binding not yet visible
+        st_volatile(&p.chunk_map[k0 + i], ok ? c + i + 1 : kChunkDone);
+    }
+    if (got) atomicAdd(&p.ws->chunks_claimed, got);
 }
 
 // Wait until local chunk k is bound (warp-collective: lane 0 reads, every lane loops on
@@ -570,20 +584,14 @@ __device__ __forceinline__ int draw_tile(const Params& p, Tile& tl, uint32_t& ck
         g = cg;
     } else {
         if (r == 0 && seg == 0) {
-            // first tile of local chunk k: bind chunk 0 if k == 0, then bind chunk k+1 one
-            // chunk ahead (claims stay in local-chunk order; chunk k is already bound when
-            // its first tile is drawn, so warps rarely wait on a claim in flight)
-            if (k == 0 && l0) {
-                const uint32_t g0 = claim_chunk(p);
-                fcfs_delay(2);
-                st_volatile(&p.chunk_map[0], g0);
-            }
+            // first tile of local chunk k: bind the first batch if k == 0; the first chunk
+            // of each batch binds the next batch one batch ahead (claims stay in
+            // local-chunk order, so once the counter is exhausted every later local chunk
+            // is too; a batch is bound before its tiles are drawn, so warps rarely wait)
+            const uint32_t nb = p.claim_batch;
+            if (k == 0 && l0) bind_chunks(p, 0, false);
             g = wait_bound(p, k);
-            if (k + 1 <= p.nchunks && l0) {
-                const uint32_t gn = g == kChunkDone ? kChunkDone : claim_chunk(p);
-                fcfs_delay(3);  // the claim is made, its binding not yet visible
-                st_volatile(&p.chunk_map[k + 1], gn);
-            }
+            if (k % nb == 0 && k + nb <= p.nchunks && l0) bind_chunks(p, k + nb, g == kChunkDone);
         } else {
             g = wait_bound(p, k);
         }

@@ -41,7 +41,8 @@ def main():
     renders, bad, kernels = 0, 0, set()
     for cfg in cfgs:
         for scheme in ("fcfs", "fcfs_master"):
-            for n in ranks:
+            # one claimant (N = 1, FCFS only) claims 16-chunk batches; the others one chunk
+            for n in ([1] if scheme == "fcfs" else []) + ranks:
                 for rep in range(a.reps):
                     out = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, device="cuda:0")
                     kernel = ["refill", "lazy2", "batch8x2", "refill1"][rep % 4]
