@@ -242,13 +242,16 @@ def run_ours(args):
             _d2h(out_host, img_ptr, nbytes, s_handle)  # rank 0 holds the whole map
         return st
 
-    def timed(scheme, steps, warmup, sampler=None, out_host=None, e2e=False, barriered=True):
+    def timed(scheme, steps, warmup, sampler=None, out_host=None, e2e=False, barriered=True, per_render=False):
         """K renders bracketed by barrier + synchronize, max over ranks (the caller reduces).
         N > 1 and barriered: a device-side barrier (rr.device_barrier: an all_reduce on the
         render stream) follows every render, so render n+1 starts on every rank only after
         every rank finished render n -- each step is one whole render to the moment rank 0
         holds the map, FCFS tail included.  barriered=False: renders follow
-        each other without a barrier (render n+1 fills render n's tail; pipelined)."""
+        each other without a barrier (render n+1 fills render n's tail; pipelined).
+        per_render: also bracket every render with its own pair of events (render_ms; a
+        separate pass -- the two event records cost the host ~8 us per step, which on a
+        small view would make the timed loop host-bound)."""
         stats = []
         for _ in range(warmup):
             step(scheme, out_host, e2e)
@@ -260,10 +263,9 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         t0 = time.time()
-        # per-render events on the launching stream: the kernel's live launch duration
-        # (each bracket also holds the render's two small state memsets)
+        # per-render events on the launching stream (per_render pass only)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(steps)] if not e2e else []
+              for _ in range(steps)] if per_render and not e2e else []
         e0.record(stream)
         for i in range(steps):
             # renders are enqueued back to back (no host round trip between them); the last
@@ -335,6 +337,8 @@ def run_ours(args):
     time.sleep(0.3)
     ms, stats = timed(args.scheme, args.steps, args.warmup, sampler)
     sampler.stop()
+    # per-render durations in a second pass (diagnostic: render_ms)
+    _, rstats = timed(args.scheme, min(args.steps, 50), 2, per_render=True)
     from paper_2007_00745_b200.multiproc import sum_over_ranks
     iters_rank = stats[-1]["sum_iters"]  # this rank's share of the last step (FCFS: varies)
     iters_launch = statistics.mean(s["sum_iters"] for s in stats)  # per launch of this rank
@@ -344,8 +348,12 @@ def run_ours(args):
     iters_job = per_step[0]
     ms_per_step = tot_ms / args.steps
     value = iters_job / (ms_per_step * 1e-3) / 1e9  # Giter/s
-    kern_ms = stats[-1]["render_ms_mean"]  # mean per-render duration over the timed region
-    kern_ms_all, _ = aggregate(dist, kern_ms, 0, adev)
+    # the escape kernel's average launch duration: at N = 1 every timed step is exactly one
+    # launch, back to back on the launching stream, so the timed region's events / K; at
+    # N > 1 a step also holds the device barrier, so the per-render event pass
+    kern_ms = ms / args.steps if world == 1 else rstats[-1]["render_ms_mean"]
+    kern_basis = ("CUDA events around the K timed launches on the launching stream / K" if world == 1 else
+                  "mean of per-render CUDA-event brackets on this rank's launching stream")
     clocks = sampler.summary()
     if clocks is not None:
         # the SM clock the escape kernels themselves measured (clock64 / %globaltimer per
@@ -367,6 +375,7 @@ def run_ours(args):
             "peak_unit_count_basis": f"{SMS} SMs x {lanes} {cfg.dtype.upper()} lanes x {SM_MAX_MHZ:.0f} MHz "
                                      "(max SM clock; DESIGN.md Roofline)",
             "kernel_ms": round(kern_ms, 4),
+            "kernel_ms_basis": kern_basis,
             "ops_per_launch": int(iters_launch * FLOPS_PER_ITER),
             "ops_per_launch_basis": f"{FLOPS_PER_ITER} FP ops (3 mul + 5 add/sub) x {iters_launch:.0f} "
                                     "pixel-iterations (sum of this rank's counts) per launch"}
@@ -397,9 +406,12 @@ def run_ours(args):
         "ms_per_step": round(ms_per_step, 4),
         # per-render CUDA-event times on rank 0's launching stream (PAPER.md:237 reports
         # repetitions; median and minimum)
-        "render_ms": {"mean": round(stats[-1]["render_ms_mean"], 4),
-                      "median": round(stats[-1]["render_ms_median"], 4),
-                      "min": round(stats[-1]["render_ms_min"], 4)},
+        "render_ms": {"mean": round(rstats[-1]["render_ms_mean"], 4),
+                      "median": round(rstats[-1]["render_ms_median"], 4),
+                      "min": round(rstats[-1]["render_ms_min"], 4),
+                      "steps": min(args.steps, 50),
+                      "note": "a second pass with an event pair around every render (the timed "
+                              "loop has events only around all K steps)"},
         "higher_is_better": True,
         "scaling": "strong" if world > 1 else "strong",
         "vs_baseline": None,

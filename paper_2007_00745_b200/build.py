@@ -104,6 +104,11 @@ def build_delay(force: bool = False) -> str:
     return out
 
 
+def build_trace(out: str = None) -> str:
+    """libmandel_trace.so: one timeline record per warp (tools/trace_view.py)."""
+    return build_debug(out, "MANDEL_TRACE=1", "libmandel_trace.so")
+
+
 def build_prof(out: str = None) -> str:
     """libmandel_prof.so: LAZY slot-state counters printed per launch (tools/lazy_prof.py)."""
     return build_debug(out, "MANDEL_LAZY_PROF=1", "libmandel_prof.so")

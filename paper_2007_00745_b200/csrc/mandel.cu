@@ -1632,4 +1632,18 @@ void mandel_shutdown(void) {
     cudaGetLastError();
 }
 
+#if MANDEL_TRACE
+// Development only (libmandel_trace.so; not in include/mandel.h): copy the first n warp
+// records of the last traced launch on the current device (tools/trace_view.py), then
+// clear them.
+int mandel_dev_trace(void* host, unsigned n) {
+    const size_t bytes = (size_t)std::min<unsigned>(n, mandel::kTraceRecs) * sizeof(mandel::TraceRec);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyFromSymbol(host, mandel::g_trace, bytes));
+    static std::vector<char> zeros(sizeof(mandel::TraceRec) * mandel::kTraceRecs, 0);
+    CK(cudaMemcpyToSymbol(mandel::g_trace, zeros.data(), zeros.size()));
+    return MANDEL_OK;
+}
+#endif
+
 }  // extern "C"

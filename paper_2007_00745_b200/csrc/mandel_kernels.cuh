@@ -75,22 +75,32 @@ constexpr uint32_t kIdleRem = 0xffffffffu;
 
 enum : uint32_t { kSchemeBlock = 0, kSchemeCyclic = 1, kSchemeFcfs = 2 };
 
-// Per-rank device state; zeroed by the host (cudaMemsetAsync) before every launch.
+// Per-rank device state; zeroed before every launch (the previous launch's first CTA,
+// zero_next_state).  Every counter the kernel updates atomically sits on its own 128-B
+// line: atomics to one line serialise in one L2 slice (~1 per cycle), and on a small
+// view the tile draws and the CTAs' closing statistics would otherwise queue behind
+// each other (C1: 16.5 us per render at iterMax 1 with one shared line).
 struct WorkState {
-    unsigned int tile_ctr;        // next local tile index
+    unsigned int tile_ctr;        // next local tile index (the tile queue: its own line)
+    unsigned int pad_t[31];
     unsigned int chunks_claimed;  // successful global FCFS claims by this rank
     unsigned int rows_started;    // rows whose first tile this rank drew
-    unsigned int pad0;
-    unsigned long long sum_iters; // sum of counts stored by this rank
-    unsigned long long pixels;    // pixels stored by this rank
+    unsigned int pad_r[30];
+    unsigned long long sum_iters; // sum of counts stored by this rank (one add per CTA)
+    unsigned long long pad_s[15];
+    unsigned long long pixels;    // pixels stored by this rank (one add per CTA)
+    unsigned long long pad_p[15];
     unsigned long long warp_iters; // inner-loop iterations summed over warps (eager/adaptive)
     unsigned long long exits;      // inner-loop exits summed over warps (eager/adaptive)
+    unsigned long long pad_l[14];
     unsigned long long clk_cycles; // sum over CTAs of thread 0's SM clock cycles (clock64) ...
     unsigned long long clk_ns;     // ... and of its wall time (%globaltimer): their ratio is the
                                    // SM clock during the kernel (mandel_stats.sm_clock_mhz)
+    unsigned long long pad_c[14];
     // followed by chunk_map[nchunks + 1] (uint32; 0 = unpublished, g+1 = global chunk g,
     // kChunkDone = exhausted)
 };
+static_assert(sizeof(WorkState) == 6 * 128, "WorkState: one 128-B line per atomic counter group");
 
 struct Params {
     double xmin, ymax, dx, dy;       // fp64 mapping constants (host-derived, step a1)
@@ -624,18 +634,9 @@ __device__ __forceinline__ void cta_clock_start(unsigned long long* sm) {
         sm[0] = (unsigned long long)clock64();
     }
 }
-__device__ __forceinline__ void cta_clock_end(const Params& p, const unsigned long long* sm) {
-    if (threadIdx.x == 0 && threadIdx.y == 0) {
-        const long long c1 = clock64();
-        const unsigned long long t1 = global_ns();
-        atomicAdd(&p.ws->clk_cycles, (unsigned long long)c1 - sm[0]);
-        atomicAdd(&p.ws->clk_ns, t1 - sm[1]);
-    }
-}
 #define MANDEL_CTA_CLOCK_START()                       \
     __shared__ unsigned long long mandel_clk_sm_[2];   \
     cta_clock_start(mandel_clk_sm_)
-#define MANDEL_CTA_CLOCK_END() cta_clock_end(p, mandel_clk_sm_)
 
 // The first CTA zeroes the next render's state half and counter word (Params::zero_next).
 __device__ __forceinline__ void zero_next_state(const Params& p) {
@@ -646,23 +647,90 @@ __device__ __forceinline__ void zero_next_state(const Params& p) {
     }
 }
 
-__device__ __forceinline__ void flush_loop_stats(const Params& p, uint32_t witers, uint32_t exits) {
-    if ((threadIdx.x & 31) == 0 && exits) {
-        atomicAdd(&p.ws->warp_iters, (unsigned long long)witers);
-        atomicAdd(&p.ws->exits, (unsigned long long)exits);
-    }
-}
-
-__device__ __forceinline__ void flush_stats(const Params& p, unsigned long long iters,
-                                            unsigned long long pix) {
+// Development timeline (-DMANDEL_TRACE=1 -> libmandel_trace.so, read by
+// tools/trace_view.py only): one record per warp -- its SM, first and last
+// %globaltimer, tiles drawn, pixels retired and their iterations.
+#ifndef MANDEL_TRACE
+#define MANDEL_TRACE 0
+#endif
+#if MANDEL_TRACE
+struct TraceRec {
+    unsigned long long t0, t1, iters;
+    unsigned int smid, tiles, pixels, warp;
+};
+constexpr uint32_t kTraceRecs = 1u << 16;
+__device__ TraceRec g_trace[kTraceRecs];
+__device__ __forceinline__ void trace_warp(unsigned long long t0, uint32_t tiles, unsigned long long iters,
+                                           unsigned long long pix) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         iters += __shfl_xor_sync(0xffffffffu, iters, o);
         pix += __shfl_xor_sync(0xffffffffu, pix, o);
     }
-    if ((threadIdx.x & 31) == 0 && pix) {
-        atomicAdd(&p.ws->sum_iters, iters);
-        atomicAdd(&p.ws->pixels, pix);
+    const uint32_t w = (blockIdx.y * gridDim.x + blockIdx.x) * kWarpsPerCta +
+                       ((threadIdx.y * blockDim.x + threadIdx.x) >> 5);
+    if ((threadIdx.x & 31) == 0 && w < kTraceRecs) {
+        unsigned int sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_trace[w] = TraceRec{t0, global_ns(), iters, sm, tiles, (unsigned int)pix, w};
+    }
+}
+#define MANDEL_TRACE_START() const unsigned long long trace_t0_ = global_ns(); uint32_t trace_tiles_ = 0
+#define MANDEL_TRACE_TILE() (++trace_tiles_)
+#define MANDEL_TRACE_END() trace_warp(trace_t0_, trace_tiles_, my_iters, my_pix)
+#else
+#define MANDEL_TRACE_START() do {} while (0)
+#define MANDEL_TRACE_TILE() do {} while (0)
+#define MANDEL_TRACE_END() do {} while (0)
+#endif
+
+// The CTA's closing statistics: each warp reduces its lanes' sums by shuffles, warp sums
+// meet in shared memory, and thread 0 adds the CTA's totals -- one atomic per counter
+// per CTA (per warp before: C1's 3552 warps x 2 adds on one line cost ~5 us), then the
+// CTA's clock span (cta_clock_start; read after the barrier, so it is the CTA's whole
+// lifetime).  witers / exits are warp-uniform (lane 0's values are the warp's).
+template <bool LOOP>
+__device__ __forceinline__ void cta_flush(const Params& p, unsigned long long iters, unsigned long long pix,
+                                          uint32_t witers, uint32_t exits, const unsigned long long* clk) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        iters += __shfl_xor_sync(0xffffffffu, iters, o);
+        pix += __shfl_xor_sync(0xffffffffu, pix, o);
+    }
+    __shared__ unsigned long long red[kWarpsPerCta][4];
+    const uint32_t tid = threadIdx.y * blockDim.x + threadIdx.x;
+    if ((tid & 31) == 0) {
+        red[tid >> 5][0] = iters;
+        red[tid >> 5][1] = pix;
+        if constexpr (LOOP) {
+            red[tid >> 5][2] = witers;
+            red[tid >> 5][3] = exits;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long a = 0, b = 0, c = 0, d = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < kWarpsPerCta; ++w) {
+            a += red[w][0];
+            b += red[w][1];
+            if constexpr (LOOP) {
+                c += red[w][2];
+                d += red[w][3];
+            }
+        }
+        if (b) {
+            atomicAdd(&p.ws->sum_iters, a);
+            atomicAdd(&p.ws->pixels, b);
+        }
+        if (LOOP && d) {
+            atomicAdd(&p.ws->warp_iters, c);
+            atomicAdd(&p.ws->exits, d);
+        }
+        const long long c1 = clock64();
+        const unsigned long long t1 = global_ns();
+        atomicAdd(&p.ws->clk_cycles, (unsigned long long)c1 - clk[0]);
+        atomicAdd(&p.ws->clk_ns, t1 - clk[1]);
     }
 }
 
@@ -697,6 +765,24 @@ __device__ __forceinline__ bool batch_key_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[
 #pragma unroll
     for (int s = 0; s < ILP; ++s) m = max(m, A::ukey(A::sumsq(x[s], y[s], x2[s], y2[s])));
     return m >= r2b;
+}
+
+// The exact replay of one slot S of a hit batch: restore its batch-start z (x from the kept
+// x + x, or sx when packed), rebuild the squares with the same operations, and run the BT
+// updates with the Eq. 2 test after each, recording the first escaping update in e[S].
+template <typename A, int ILP, int BT, int S, typename T, typename B>
+__device__ __forceinline__ void replay_slot(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
+                                            const T (&cr)[ILP], const T (&ci)[ILP], const T (&t0)[ILP],
+                                            const T (&sx)[ILP], const T (&sy)[ILP], B r2, uint32_t (&e)[ILP]) {
+    if constexpr (A::kPacked) x[S] = sx[S];
+    else x[S] = A::half(t0[S]);
+    y[S] = sy[S];
+    A::resq(x[S], y[S], x2[S], y2[S]);
+#pragma unroll
+    for (int u = 0; u < BT; ++u) {
+        A::step(x[S], y[S], x2[S], y2[S], cr[S], ci[S]);
+        if (A::bits(A::sumsq(x[S], y[S], x2[S], y2[S])) > r2) e[S] = min(e[S], (uint32_t)u);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -760,20 +846,33 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                 if (hit) k -= BT;      // ... which is counted after its replay
                 if (!hit) break;
                 uint32_t e[ILP];  // the slot's first escaping update in the batch (BT: none)
+                // per slot index: R18 holds slot by slot (a slot whose final key stayed below
+                // r2b did not escape in the batch), so with ILP 2 a hit confined to one slot
+                // index replays that slot alone -- the other keeps its batch-end state
+                bool hs[ILP];
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) {
-                    if constexpr (A::kPacked) x[s] = sx[s];
-                    else x[s] = A::half(t0[s]);  // (x + x) * 0.5 = x exactly
-                    y[s] = sy[s];
-                    A::resq(x[s], y[s], x2[s], y2[s]);
+                    hs[s] = ILP == 1 || __any_sync(FULL, A::ukey(A::sumsq(x[s], y[s], x2[s], y2[s])) >= r2b);
                     e[s] = BT;
                 }
-#pragma unroll
-                for (int u = 0; u < BT; ++u) {
+                if (ILP == 2 && !(hs[0] && hs[1])) {
+                    if (hs[0]) replay_slot<A, ILP, BT, 0>(x, y, x2, y2, cr, ci, t0, sx, sy, r2, e);
+                    else replay_slot<A, ILP, BT, ILP - 1>(x, y, x2, y2, cr, ci, t0, sx, sy, r2, e);
+                } else {
 #pragma unroll
                     for (int s = 0; s < ILP; ++s) {
-                        A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
-                        if (A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2) e[s] = min(e[s], (uint32_t)u);
+                        if constexpr (A::kPacked) x[s] = sx[s];
+                        else x[s] = A::half(t0[s]);  // (x + x) * 0.5 = x exactly
+                        y[s] = sy[s];
+                        A::resq(x[s], y[s], x2[s], y2[s]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < BT; ++u) {
+#pragma unroll
+                        for (int s = 0; s < ILP; ++s) {
+                            A::step(x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
+                            if (A::bits(A::sumsq(x[s], y[s], x2[s], y2[s])) > r2) e[s] = min(e[s], (uint32_t)u);
+                        }
                     }
                 }
                 bool any_esc = false;
@@ -854,6 +953,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     MANDEL_CTA_CLOCK_START();
+    MANDEL_TRACE_START();
     zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
@@ -914,6 +1014,7 @@ escape_refill_kernel(const Params p) {
                     const int st = draw_tile(p, tl, ck_, cg_, tn_);  // warp-uniform
                     if (st == kTileNone) { more = false; break; }
                     if (st == kTileSkip) continue;
+                    MANDEL_TRACE_TILE();
                     tq = 0;
                     tqend = tl.nrows * tl.cols;
                     tile_e0 = (tile_e0 + sub_open) & (kStageEntries - 1);
@@ -994,9 +1095,8 @@ escape_refill_kernel(const Params p) {
         }
     }
     if (STAGE) stage_drain(p, ring, lane);
-    flush_stats(p, my_iters, my_pix);
-    if (LSTATS) flush_loop_stats(p, w_iters, w_exits);
-    MANDEL_CTA_CLOCK_END();
+    MANDEL_TRACE_END();
+    cta_flush<LSTATS>(p, my_iters, my_pix, w_iters, w_exits, mandel_clk_sm_);
 }
 
 // ---------------------------------------------------------------------------
@@ -1053,6 +1153,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_lazy_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     MANDEL_CTA_CLOCK_START();
+    MANDEL_TRACE_START();
     zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
@@ -1114,6 +1215,7 @@ escape_lazy_kernel(const Params p) {
                 const int st = draw_tile(p, tl, ck_, cg_, tn_);  // warp-uniform
                 if (st == kTileNone) { more = false; break; }
                 if (st == kTileSkip) continue;
+                MANDEL_TRACE_TILE();
                 tq = 0;
                 tqend = tl.nrows * tl.cols;
                 tile_e0 = (tile_e0 + sub_open) & (kStageEntries - 1);
@@ -1218,8 +1320,8 @@ escape_lazy_kernel(const Params p) {
         }
     }
 #endif
-    flush_stats(p, my_iters, my_pix);
-    MANDEL_CTA_CLOCK_END();
+    MANDEL_TRACE_END();
+    cta_flush<false>(p, my_iters, my_pix, 0u, 0u, mandel_clk_sm_);
 }
 
 // ---------------------------------------------------------------------------
@@ -1245,6 +1347,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_adaptive_kernel(const Params p) {
     MANDEL_DCHECK((reinterpret_cast<uintptr_t>(p.ws) & 7u) == 0 && p.tile_rows >= 1 && p.tile_w >= 1);
     MANDEL_CTA_CLOCK_START();
+    MANDEL_TRACE_START();
     zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
@@ -1295,6 +1398,7 @@ escape_adaptive_kernel(const Params p) {
                     const int st = draw_tile(p, tl, ck_, cg_, tn_);  // warp-uniform
                     if (st == kTileNone) { more = false; break; }
                     if (st == kTileSkip) continue;
+                    MANDEL_TRACE_TILE();
                     tq = 0;
                     tqend = tl.nrows * tl.cols;
                 }
@@ -1392,8 +1496,8 @@ escape_adaptive_kernel(const Params p) {
             need[s] = __ballot_sync(FULL, done);
         }
     }
-    flush_stats(p, my_iters, my_pix);
-    MANDEL_CTA_CLOCK_END();
+    MANDEL_TRACE_END();
+    cta_flush<false>(p, my_iters, my_pix, 0u, 0u, mandel_clk_sm_);
 }
 
 #undef ADAPT_LAZY_STEP_SLOT
@@ -1407,6 +1511,7 @@ template <typename AR>
 __global__ void __launch_bounds__(kCtaThreads)
 escape_static_kernel(const Params p) {
     MANDEL_CTA_CLOCK_START();
+    MANDEL_TRACE_START();
     zero_next_state(p);
     typedef AR A;
     typedef typename AR::T T;
@@ -1433,8 +1538,8 @@ escape_static_kernel(const Params p) {
         my_pix = 1;
         if (threadIdx.x == 0 && j == 0) atomicAdd(&p.ws->rows_started, 1u);
     }
-    flush_stats(p, my_iters, my_pix);
-    MANDEL_CTA_CLOCK_END();
+    MANDEL_TRACE_END();
+    cta_flush<false>(p, my_iters, my_pix, 0u, 0u, mandel_clk_sm_);
 }
 
 #undef MANDEL_STEP
