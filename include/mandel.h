@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 7
+#define MANDEL_ABI_VERSION 8
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -137,6 +137,8 @@ typedef struct mandel_stats {
                                       stores), 1 staged 8 x 8 blocks stored count by count, 2 staged
                                       blocks stored with 16-B vector stores (map 16-B aligned, W and
                                       the tile width multiples of 4)                               */
+    int32_t  fused_y;              /* 1: the fused-y form was enabled for rank 0's launch (its warps
+                                      use it where their pixels allow, options.fused_y)         */
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
@@ -195,6 +197,13 @@ typedef struct mandel_options {
                                 gather's NVLink peer stores), direct into the rank's own HBM    */
     int      ctas_per_sm;    /* persistent kernels: at most this many resident CTAs per SM (grid =
                                 min(this, occupancy) x SMs); 0 -> the occupancy maximum            */
+    int      fused_y;        /* fp64 / fp32, EAGER and LAZY kernels: how y' = (x + x) y + ci is
+                                evaluated (R21).  0 or 1 -> fma(RN(x y), 2, ci) for the
+                                warps whose pixels are all "safe" (cr != 0, |cr| and any nonzero
+                                |ci| >= 2^-400 [fp32 2^-32]) when R^2 <= 2^256 [fp32 2^64]: the
+                                same rounded value, one instruction fewer per update; other
+                                warps and views use the three-operation form.  -1 -> always the
+                                three-operation form.  Counts are identical either way.        */
 } mandel_options;
 
 /*

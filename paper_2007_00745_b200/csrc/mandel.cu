@@ -334,6 +334,7 @@ struct KernelChoice {
     int bt;          // EAGER: z-updates per escape check (1 = every update; 4, 8, 16 = batched, R18)
     int packed = 0;  // fp32 batched loop on FADD2/FMUL2 slot pairs (set by build_params)
     int ctas = 0;    // resident CTAs per SM cap (0: the occupancy maximum)
+    int lanes = 0;   // LAZY refill_lanes (0: kDefaultRefillLanes; options.refill_lanes wins)
 };
 // ILP2 runs with ptxas' unconstrained schedule (74 registers, 3 CTAs of 256 threads per SM).
 // Batched escape check with a whole-batch replay on a hit (R18), measured per config
@@ -597,13 +598,28 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
         ls.fn = kernel_fn(packed ? 3 : fi, kc.variant, kc.ilp, mi, kc.bt);
     }
     p.opaque_zero = 0u;
+    // fused-y form (R21): exact while |x y| <= R^2 cannot overflow 2 RN(x y) --
+    // R^2 <= 2^256 (fp64) / 2^64 (fp32); the kernels add the per-pixel condition
+    const int fy = o ? o->fused_y : 0;
+    if (fy < -1 || fy > 1) return fail(MANDEL_EINVAL, "options.fused_y must be -1, 0 or 1");
+    double r2v;
+    if (dtype == MANDEL_FP32) {
+        float f;
+        const int32_t b = (int32_t)d.r2bits;
+        std::memcpy(&f, &b, 4);
+        r2v = f;
+    } else {
+        std::memcpy(&r2v, &d.r2bits, 8);
+    }
+    p.fused_y = (fy >= 0 && r2v <= (dtype == MANDEL_FP32 ? 0x1p64 : 0x1p256)) ? 1u : 0u;
     p.band = (o && o->band_out) ? 1u : 0u;
     p.stage = stage ? 1u : 0u;
     p.vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15u) == 0 && (W & 3u) == 0 && (tile & 3u) == 0) ? 1u : 0u;
     p.out_rows = p.band ? 0u : H;  // a band's capacity is the caller's (not known here)
     if (!ls.fn) return fail(MANDEL_EINVAL, "no kernel instantiated for this variant/ilp/min_ctas");
     const bool persistent = kc.variant != MANDEL_KERNEL_STATIC;  // (the probe variant is persistent)
-    int rl = (o && o->refill_lanes) ? o->refill_lanes : (int)kDefaultRefillLanes;
+    int rl = (o && o->refill_lanes) ? o->refill_lanes
+                                    : (kc.lanes ? kc.lanes : (int)kDefaultRefillLanes);
     if (rl < 1 || rl > 32) return fail(MANDEL_EINVAL, "options.refill_lanes must be in 1..32");
     p.refill_lanes = (uint32_t)rl;
     p.adapt_lo = (o && o->adapt_lo > 0) ? (uint32_t)o->adapt_lo : kDefaultAdaptLo;
@@ -723,30 +739,13 @@ float g_probe[2] = {0, 0};  // last probe: eager sample time (ms), eager iterati
 // the previous threshold (10, set against the per-update EAGER loop) lost up to 1.7x.
 constexpr float kLazyBelowItersPerExit = 23.0f;
 constexpr uint32_t kProbeStride = 16;
+constexpr uint64_t kTunePixels = 1ull << 21;  // views up to 2 M pixels are tuned by timing
 
 // The probe renders its sample rows into a compact band in library-owned scratch memory
 // on the probing device (band mode: band row = sample index), never into the caller's
 // map -- under mandel_render_rank that map is rank 0's shared image on another GPU.
-int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, uint32_t iter_max,
-                int dtype, const mandel_options* o, size_t state_cap, int device, cudaStream_t s,
-                KernelChoice& out) {
-    const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
-    out = kDefaultChoice[fi];
-    if (o && (o->kernel != MANDEL_KERNEL_REFILL || o->ilp || o->min_ctas > 1)) return MANDEL_OK;
-    // too small to matter (below ~0.5 M pixels a render is a few tens of microseconds);
-    // C1 (800^2) is probed: LAZY's exact per-update record suits its short counts
-    if (H < 32 * kProbeStride || (uint64_t)W * H < (1u << 19)) return MANDEL_OK;
-    ViewKey key{{bounds[0], bounds[1], bounds[2], bounds[3], bounds[4]}, W, H, iter_max, dtype};
-    auto it = g_auto.find(key);
-    if (it != g_auto.end()) {
-        out = it->second;
-        return MANDEL_OK;
-    }
-    const uint32_t n = (H + kProbeStride - 1) / kProbeStride;
-    const Plan pl{n, 0, kProbeStride, n, 0};
-    DeviceCtx& dc = g_dev[device];
-    const size_t sbytes = (size_t)n * W * sizeof(uint32_t);
-    CK(cudaSetDevice(device));
+// The probe's device buffers: a compact output band of sbytes and its own work state.
+int ensure_probe_buffers(DeviceCtx& dc, size_t sbytes, size_t state_cap) {
     if (dc.scratch_bytes < sbytes) {
         if (dc.scratch) {
             CK(cudaDeviceSynchronize());
@@ -767,6 +766,97 @@ int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, 
         CK(cudaMalloc(&dc.pstate, state_cap));
         dc.pstate_bytes = state_cap;
     }
+    return MANDEL_OK;
+}
+
+// Small views (<= kTunePixels): render the whole view once with each candidate kernel into
+// the probe's scratch (whole GPU, row order, one rank), twice each, and keep the fastest.
+// A small render is latency- and tail-bound, so the iterations-per-exit statistic that
+// picks EAGER or LAZY on large views does not predict it, and a 1/16 sample does not either
+// (DESIGN.md); the whole view costs only a few of its own renders, once per view.  The
+// candidates: the batched EAGER default, EAGER with the other slot count, LAZY ILP 2
+// (refill at 16 free lanes), LAZY ILP 1 refilling only whole warps (32) -- measured over six
+// small views, each is the best on some (profiles/r02af_small_views.jsonl).  Any choice
+// computes the same counts.
+int tune_small(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, int dtype,
+               const mandel_options* o, size_t state_cap, int device, cudaStream_t s, KernelChoice& out) {
+    const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
+    DeviceCtx& dc = g_dev[device];
+    CK(cudaSetDevice(device));
+    int rc = ensure_probe_buffers(dc, (size_t)W * H * sizeof(uint32_t), state_cap);
+    if (rc) return rc;
+    const Plan pl{H, 0, 1, H, 0};
+    KernelChoice cand[4] = {kDefaultChoice[fi], kDefaultChoice[fi], {MANDEL_KERNEL_LAZY, 2, 1, 1},
+                            {MANDEL_KERNEL_LAZY, 1, 1, 1}};
+    cand[1].ilp = kDefaultChoice[fi].ilp == 1 ? 2 : 1;
+    cand[1].minb = 1;
+    cand[1].ctas = 0;
+    cand[2].lanes = (int)kDefaultRefillLanes;
+    cand[3].lanes = 32;
+    mandel_options po{};
+    if (o) po = *o;
+    po.max_sms = 0;   // the view, not the launch geometry (as the probe)
+    po.band_out = 1;  // view row k -> scratch row k
+    cudaEvent_t ev[8];
+    for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&ev[i]));
+    float best[4] = {1e30f, 1e30f, 1e30f, 1e30f};
+    for (int round = 0; round < 3 && rc == MANDEL_OK; ++round) {
+        for (int c = 0; c < 4 && rc == MANDEL_OK; ++c) {
+            LaunchSpec ls;
+            rc = build_params(d, W, H, iter_max, dtype, MANDEL_BLOCK, 1, 0, &po, dc.scratch, dc.pstate, state_cap,
+                              nullptr, false, device, ls, &pl, &cand[c]);
+            if (rc) break;
+            if (cudaMemsetAsync(dc.pstate, 0, state_cap, s) != cudaSuccess) { rc = cuda_fail(cudaGetLastError(), "tune memset"); break; }
+            cudaEventRecord(ev[2 * c], s);
+            rc = launch(ls, s);
+            cudaEventRecord(ev[2 * c + 1], s);
+        }
+        if (rc) break;
+        if (cudaStreamSynchronize(s) != cudaSuccess) { rc = cuda_fail(cudaGetLastError(), "tune sync"); break; }
+        for (int c = 0; c < 4 && round > 0; ++c) {  // round 0 warms every candidate
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[2 * c], ev[2 * c + 1]);
+            best[c] = std::min(best[c], ms);
+        }
+    }
+    for (int i = 0; i < 8; ++i) cudaEventDestroy(ev[i]);
+    if (rc) return rc;
+    int k = 0;
+    for (int c = 1; c < 4; ++c)
+        if (best[c] < best[k]) k = c;
+    out = cand[k];
+    g_probe[0] = best[k];
+    g_probe[1] = 0.f;  // no iterations-per-exit statistic: timed
+    return MANDEL_OK;
+}
+
+int auto_choice(const Derived& d, const double* bounds, uint32_t W, uint32_t H, uint32_t iter_max,
+                int dtype, const mandel_options* o, size_t state_cap, int device, cudaStream_t s,
+                KernelChoice& out) {
+    const int fi = dtype == MANDEL_FP32 ? 1 : (dtype == MANDEL_FP64_FMA ? 2 : 0);
+    out = kDefaultChoice[fi];
+    if (o && (o->kernel != MANDEL_KERNEL_REFILL || o->ilp || o->min_ctas > 1)) return MANDEL_OK;
+    ViewKey key{{bounds[0], bounds[1], bounds[2], bounds[3], bounds[4]}, W, H, iter_max, dtype};
+    auto it = g_auto.find(key);
+    if (it != g_auto.end()) {
+        out = it->second;
+        return MANDEL_OK;
+    }
+    // small views: time the candidates on the view itself, once (tune_small)
+    if ((uint64_t)W * H <= kTunePixels) {
+        int rc = tune_small(d, W, H, iter_max, dtype, o, state_cap, device, s, out);
+        if (rc) return rc;
+        g_auto[key] = out;
+        return MANDEL_OK;
+    }
+    if (H < 32 * kProbeStride) return MANDEL_OK;
+    const uint32_t n = (H + kProbeStride - 1) / kProbeStride;
+    const Plan pl{n, 0, kProbeStride, n, 0};
+    DeviceCtx& dc = g_dev[device];
+    const size_t sbytes = (size_t)n * W * sizeof(uint32_t);
+    CK(cudaSetDevice(device));
+    int rc0 = ensure_probe_buffers(dc, sbytes, state_cap);
+    if (rc0) return rc0;
     void* const pst = dc.pstate;
     const KernelChoice cand[2] = {{kVariantProbe, kDefaultChoice[fi].ilp, kDefaultChoice[fi].minb, 1},
                                   {MANDEL_KERNEL_LAZY, 2, 1, 1}};
@@ -980,6 +1070,7 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         stats->kernel_batch = specs[0].kc.bt;
         stats->kernel_packed = specs[0].kc.packed;
         stats->store_mode = store_mode(specs[0].p);
+        stats->fused_y = (int32_t)specs[0].p.fused_y;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -1204,6 +1295,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         stats->kernel_batch = specs[0].kc.bt;
         stats->kernel_packed = specs[0].kc.packed;
         stats->store_mode = store_mode(specs[0].p);
+        stats->fused_y = (int32_t)specs[0].p.fused_y;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -1410,6 +1502,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->kernel_batch = ls.kc.bt;
         stats->kernel_packed = ls.kc.packed;
         stats->store_mode = store_mode(ls.p);
+        stats->fused_y = (int32_t)ls.p.fused_y;
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t0;

@@ -110,6 +110,7 @@ struct Params {
     uint32_t r2batch;                // batched-check threshold on ukey, below key(R2) (R18)
     uint32_t W, H, iter_max;
     uint32_t scheme;
+    uint32_t fused_y;                // 1: warps whose slots are all safe run the fused-y form (R21)
     uint32_t tile_w, tiles_per_row;  // columns per tile; tiles per group of tile_rows row slots
     uint32_t tile_rows;              // row slots per tile (FCFS: divides chunk_rows)
     uint32_t tile_shift;             // log2(tile_rows * 8)
@@ -257,6 +258,52 @@ struct ArithF32 {
         y2 = mul(y, y);
     }
 };
+
+// ---------------------------------------------------------------------------
+// "Fused-y" forms of the fp64 / fp32 policies (R21): the same map, one FP
+// instruction fewer per update.  Eq. 1's y' = RN(RN((x + x) y) + ci) is computed as
+// fma(RN(x y), 2, ci) = RN(2 RN(x y) + ci): x + x is exact, and RN(2p) = 2 RN(p) for
+// any product p in the normal range, so the two agree whenever x y is 0 or normal and
+// 2 RN(x y) does not overflow.  A slot may run this form only when its pixel is "safe":
+// cr != 0 with |cr| >= 2^-400 and (ci = 0 or |ci| >= 2^-400) [fp32: 2^-32], and R^2 <= 2^256
+// [fp32: 2^64].  Then every iterate component before the escape is 0 or at least
+// 2^-454 (the sum of two doubles >= 2^-401 in magnitude is 0 or a multiple of their
+// common ulp), so |x y| is 0 or >= 2^-908 (normal), and |x y| <= R^2 (no overflow).
+// The kernels check the pixels of a warp at every refill (fast_slot) and run a warp's
+// loop in this form only when all of its live slots are safe; the replay of a hit batch
+// uses the same form (exact before the escape, so the recorded escape is the oracle's).
+// ---------------------------------------------------------------------------
+struct ArithF64Y : ArithF64 {
+    static __device__ __forceinline__ void step(double& x, double& y, double& x2, double& y2,
+                                                double cr, double ci) {
+        const double ny = __fma_rn(mul(x, y), 2.0, ci);
+        const double nx = add(sub(x2, y2), cr);
+        x = nx;
+        y = ny;
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
+    static __device__ __forceinline__ bool fast_slot(double cr, double ci) {
+        return fabs(cr) >= 0x1p-400 && (ci == 0.0 || fabs(ci) >= 0x1p-400);
+    }
+};
+struct ArithF32Y : ArithF32 {
+    static __device__ __forceinline__ void step(float& x, float& y, float& x2, float& y2, float cr, float ci) {
+        const float ny = __fmaf_rn(mul(x, y), 2.0f, ci);
+        const float nx = add(sub(x2, y2), cr);
+        x = nx;
+        y = ny;
+        x2 = mul(x, x);
+        y2 = mul(y, y);
+    }
+    static __device__ __forceinline__ bool fast_slot(float cr, float ci) {
+        return fabsf(cr) >= 0x1p-32f && (ci == 0.0f || fabsf(ci) >= 0x1p-32f);
+    }
+};
+// The fused-y partner of a policy (itself where there is none).
+template <typename A> struct FusedY { typedef A type; static constexpr bool kHas = false; };
+template <> struct FusedY<ArithF64> { typedef ArithF64Y type; static constexpr bool kHas = true; };
+template <> struct FusedY<ArithF32> { typedef ArithF32Y type; static constexpr bool kHas = true; };
 
 // MANDEL_FP32 with the batched loop on packed pairs of slots (NEXT-4b): FADD2/FMUL2
 // (PTX add/sub/mul.rn.f32x2, sm_100a) do two slots' RN operations per instruction,
@@ -968,9 +1015,12 @@ escape_refill_kernel(const Params p) {
     uint32_t rem[ILP];
     uint32_t* dst[ILP];
     uint32_t stag[ILP];  // the slot's staging tag (entry * 64 + pixel of the block) or kStageDirect
+    bool fs[ILP];        // the slot may run the fused-y form (FusedY; idle slots may)
+    typedef typename FusedY<A>::type AF;
 #pragma unroll
     for (int s = 0; s < ILP; ++s) {
         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+        fs[s] = true;
         rem[s] = kIdleRem;
         dst[s] = p.out;
         stag[s] = kStageDirect;
@@ -1037,6 +1087,7 @@ escape_refill_kernel(const Params p) {
                         tile_pixel(p, tl, tq + q, i, j, o, sb, w);
                         cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));      // Cx[j] = xmin + j*dx
                         ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));      // Cy[i] = ymax - i*dy
+                        if constexpr (FusedY<A>::kHas) fs[s] = AF::fast_slot(cr[s], ci[s]);
                         x[s] = y[s] = x2[s] = y2[s] = zero;
                         rem[s] = p.iter_max;
                         const bool stg = STAGE && sb < sub_open;
@@ -1054,6 +1105,7 @@ escape_refill_kernel(const Params p) {
                 for (int s = 0; s < ILP; ++s) {
                     if (((need[s] >> lane) & 1u) && rank[s] >= served) {
                         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+                        fs[s] = true;
                         rem[s] = kIdleRem;
                     }
                 }
@@ -1067,7 +1119,16 @@ escape_refill_kernel(const Params p) {
 
         bool fin[ILP];
         uint32_t kx[ILP];  // per-slot iterations of this run (differs from k for batch-replay escapes)
-        const uint32_t k = eager_run<A, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax);
+        // the fused-y form when every slot of the warp is safe for it (ArithF64Y)
+        bool fast = false;
+        if constexpr (FusedY<A>::kHas) {
+            bool ok = p.fused_y != 0u;
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) ok = ok && fs[s];
+            fast = __all_sync(FULL, ok);
+        }
+        const uint32_t k = fast ? eager_run<AF, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax)
+                                : eager_run<A, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax);
 
         if (LSTATS) {
             w_iters += k;
@@ -1173,9 +1234,12 @@ escape_lazy_kernel(const Params p) {
     bool has[ILP];   // the slot holds a pixel not yet stored (else idle: z = c = 0)
     uint32_t* dst[ILP];
     uint32_t stag[ILP];  // staging tag (as escape_refill_kernel)
+    bool fs[ILP];        // the slot may run the fused-y form (FusedY; idle slots may)
+    typedef typename FusedY<A>::type AF;
 #pragma unroll
     for (int s = 0; s < ILP; ++s) {
         x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;
+        fs[s] = true;
         n[s] = 0;
         live[s] = has[s] = false;
         dst[s] = p.out;
@@ -1235,6 +1299,7 @@ escape_lazy_kernel(const Params p) {
                     tile_pixel(p, tl, tq + (rank[s] - served), i, j, o, sb, w);
                     cr[s] = A::add(xmin, A::mul(A::cvt(j), dx));  // Cx[j] = xmin + j*dx
                     ci[s] = A::sub(ymax, A::mul(A::cvt(i), dy));  // Cy[i] = ymax - i*dy
+                    if constexpr (FusedY<A>::kHas) fs[s] = AF::fast_slot(cr[s], ci[s]);
                     x[s] = y[s] = x2[s] = y2[s] = zero;
                     n[s] = 0;
                     live[s] = has[s] = true;
@@ -1250,6 +1315,15 @@ escape_lazy_kernel(const Params p) {
 #pragma unroll
         for (int s = 0; s < ILP; ++s) any_live |= live[s];
         if (!__any_sync(FULL, any_live)) break;  // tiles exhausted and every slot retired
+        // the fused-y form when every live slot of the warp is safe for it (ArithF64Y);
+        // finished slots iterate unread and idle ones hold z = c = 0
+        bool fast = false;
+        if constexpr (FusedY<A>::kHas) {
+            bool ok = p.fused_y != 0u;
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) ok = ok && (fs[s] || !live[s]);
+            fast = __all_sync(FULL, ok);
+        }
 #if MANDEL_LAZY_PROF
         prof[more ? 6 : 7] += 1;
 #endif
@@ -1257,7 +1331,8 @@ escape_lazy_kernel(const Params p) {
         // ---- blocks of LU updates until enough slots have finished
         for (;;) {
             uint32_t e[ILP];
-            lazy_block<A, ILP, LU>(x, y, x2, y2, cr, ci, r2, e);
+            if (fast) lazy_block<AF, ILP, LU>(x, y, x2, y2, cr, ci, r2, e);
+            else lazy_block<A, ILP, LU>(x, y, x2, y2, cr, ci, r2, e);
             bool fin[ILP];
 #pragma unroll
             for (int s = 0; s < ILP; ++s) {
@@ -1296,6 +1371,7 @@ escape_lazy_kernel(const Params p) {
                 my_iters += n[s];
                 my_pix += 1;
                 has[s] = false;
+                fs[s] = true;
                 x[s] = y[s] = x2[s] = y2[s] = cr[s] = ci[s] = zero;  // idle: z = 0 forever
             }
         }

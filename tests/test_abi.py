@@ -30,20 +30,27 @@ def test_library_is_sm100a_only(mandel):
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", mandel.LIB_PATH], capture_output=True,
                           text=True).stdout
-    # no FMA contraction in any kernel except the explicit FMA dtype's (R10, R17)
-    fn, fma_fns = None, 0
+    # no FMA contraction in any kernel except the explicit FMA dtype's (R10, R17);
+    # elsewhere the only FMA is the fused-y form fma(RN(x y), 2, ci) (R21): an exact doubling
+    # of its first operand, the immediate 2 -- never a contracted multiply-add pair
+    import re
+    fn, fma_fns, fused = None, 0, 0
+    doubling = re.compile(r"\b[DF]FMA R\d+, R\d+(\.reuse)?, 2, R\d+(\.reuse)? ;")
     for line in sass.splitlines():
         if "Function :" in line:
             fn = line.split("Function :")[1].strip()
             continue
         if "DFMA" in line or "FFMA" in line:
-            assert fn and "ArithF64Fma" in fn, (fn, line)
-            fma_fns += 1
-    assert fma_fns > 0
+            if fn and "ArithF64Fma" in fn:
+                fma_fns += 1
+            else:
+                assert doubling.search(line), (fn, line)
+                fused += 1
+    assert fma_fns > 0 and fused > 0
 
 
 def test_abi_version_and_strerror(mandel):
-    assert mandel.mandel_abi_version() == 7
+    assert mandel.mandel_abi_version() == 8
     for code in range(-7, 1):
         assert mandel.strerror(code) and mandel.strerror(code) != "unknown status"
 

@@ -234,11 +234,12 @@ def test_fp32_packed_loop(mandel, oracle, kernel):
 
 @pytest.mark.parametrize("R,batch", [(2.0, 8), (1.9999999999999998, 1), (1.5, 1), (20.0, 8)])
 def test_batched_check_default_and_fallback(mandel, oracle, R, batch):
-    # default kernel: batched when R >= 2, the per-update test otherwise (same map either way)
+    # the default EAGER loop (an explicit ilp skips the per-view choice, which may pick LAZY):
+    # batched when R >= 2, the per-update test otherwise (same map either way)
     cfg = wl.C1.with_(W=300, H=200, R=R)
-    out, st = _render_dev(mandel, cfg, "fcfs", 1)
+    out, st = _render_dev(mandel, cfg, "fcfs", 1, ilp=2)
     _assert_same(_host(out), oracle.render(cfg), f"default R={R}")
-    assert st["kernel_batch"] == batch
+    assert st["kernel"] == "eager" and st["kernel_batch"] == batch
     if batch == 1:
         with pytest.raises(mandel.MandelError):
             _render_dev(mandel, cfg, "fcfs", 1, check_every=4)
@@ -743,3 +744,86 @@ def test_back_to_back_renders_reset_state_in_kernel(mandel, oracle):
             out, st = _render_dev(mandel, v, scheme, n)
             _assert_same(_host(out), w, f"stats {scheme}/{n}")
             assert st["chunks_claimed"] == -(-v.H // 16) and st["pixels"] == v.pixels
+
+
+@pytest.mark.parametrize("dtype", ["fp64", "fp32", "fp64fma"])
+def test_small_view_tuning(mandel, oracle, dtype):
+    """Views up to 2^21 pixels pick their kernel by timing the candidates on the view
+    itself, once (tune_small): whatever wins, the map is the oracle's, the choice is cached
+    per view (the second render reports the same kernel), and it applies to every scheme
+    and rank count."""
+    mandel.mandel_shutdown()  # clears the per-view cache
+    cfg = wl.C1.with_(W=700, H=500, iter_max=400, dtype=dtype)
+    want = oracle.render(cfg)
+    out, st = _render_dev(mandel, cfg, "block", 1)
+    _assert_same(_host(out), want, f"tuned {dtype}")
+    assert st["kernel"] in ("eager", "lazy")
+    assert st["probe"][1] == 0.0 and st["probe"][0] > 0  # timed, not the ipe statistic
+    first = (st["kernel"], st["kernel_ilp"])
+    for scheme, n in (("block", 1), ("cyclic", 3), ("fcfs", 2), ("fcfs", 1)):
+        out, st = _render_dev(mandel, cfg, scheme, n)
+        _assert_same(_host(out), want, f"tuned {dtype} {scheme}/N={n}")
+        assert (st["kernel"], st["kernel_ilp"]) == first
+    # an SM-sliced render tunes on the whole GPU and still renders the view exactly
+    mandel.mandel_shutdown()
+    out, st = _render_dev(mandel, cfg, "block", 1, max_sms=3)
+    _assert_same(_host(out), want, f"tuned {dtype} max_sms")
+
+
+# ---------------------------------------------------------------------------
+# fused-y form (DESIGN.md R21): y' = fma(RN(x y), 2, ci) where it equals the oracle's
+# RN(RN((x + x) y) + ci); unsafe pixels (cr = 0, tiny |c| components) and views with a
+# huge R keep the three-operation form -- maps identical to the oracle either way
+# ---------------------------------------------------------------------------
+FUSED_VIEWS = {
+    "c1": wl.C1.with_(W=400, H=300, iter_max=300),
+    # a column at cr = 0 exactly (and a row at ci = 0)
+    "zero_column": wl.Config("zc", -1.0, 1.0, -1.0, 1.0, 64, 64, 500, 2.0, "fp64"),
+    # every |c| component below 2^-400 (fp64) / 2^-32 (fp32): all pixels take the exact form
+    "tiny": wl.Config("tiny", -1e-125, 1e-125, -1e-125, 1e-125, 48, 40, 200, 2.0, "fp64"),
+    "tiny32": wl.Config("tiny32", -1e-11, 1e-11, -1e-11, 1e-11, 48, 40, 200, 2.0, "fp64"),
+    # a mix: columns either side of the 2^-400 bound in one tile
+    "mixed": wl.Config("mix", -4e-120, 4e-120, -0.5, 0.5, 96, 64, 300, 2.0, "fp64"),
+    # near the c = -2 tip and the real axis (|z| = 2 orbits, exact R^2 hits)
+    "tip": wl.Config("tip", -2.0, -1.9, -0.05, 0.05, 128, 96, 1000, 2.0, "fp64"),
+    # fp32's bound (2^-32) inside one tile
+    "mixed32": wl.Config("mix32", -1e-9, 1e-9, -0.5, 0.5, 96, 64, 300, 2.0, "fp64"),
+}
+FP64_ONLY = ("tiny", "mixed")  # windows below fp32's range (they collapse to 0 in fp32)
+
+
+@pytest.mark.parametrize("view", sorted(FUSED_VIEWS))
+@pytest.mark.parametrize("kernel", ["refill", "lazy1", "lazy2", "batch8x1", "batch8x2", "refill1", "batch4x2"])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_fused_y_parity(mandel, oracle, view, kernel, dtype):
+    if dtype == "fp32" and view in FP64_ONLY:
+        return  # not representable in fp32 (covered by tiny32 / mixed32)
+    cfg = FUSED_VIEWS[view].with_(dtype=dtype)
+    want = oracle.render(cfg)
+    for fy in (0, -1):
+        out, st = _render_dev(mandel, cfg, "block", 1, kernel=kernel, fused_y=fy)
+        _assert_same(_host(out), want, f"fused_y={fy}/{view}/{kernel}/{dtype}")
+        assert st["fused_y"] == (1 if fy == 0 else 0)
+
+
+@pytest.mark.parametrize("dtype,R,on", [("fp64", 2.0 ** 128, 1), ("fp64", 2.0 ** 128 * 1.5, 0),
+                                        ("fp32", 2.0 ** 32, 1), ("fp32", 2.0 ** 32 * 1.5, 0)])
+def test_fused_y_needs_bounded_r(mandel, oracle, dtype, R, on):
+    # R^2 <= 2^256 (fp64) / 2^64 (fp32) keeps 2 RN(x y) finite before the escape
+    cfg = wl.C1.with_(W=120, H=90, iter_max=60, R=R, dtype=dtype)
+    out, st = _render_dev(mandel, cfg, "cyclic", 2, kernel="lazy2")
+    _assert_same(_host(out), oracle.render(cfg), f"R={R}/{dtype}")
+    assert st["fused_y"] == on
+    with pytest.raises(mandel.MandelError):
+        _render_dev(mandel, cfg, "block", 1, fused_y=2)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_fused_y_whole_map_matches_exact_form(mandel, name):
+    # the whole bench map with and without the fused-y form, element by element
+    cfg = wl.CONFIGS[name]
+    a, sa = _render_dev(mandel, cfg, "block", 1, fused_y=0)
+    b, sb = _render_dev(mandel, cfg, "block", 1, fused_y=-1)
+    assert sa["fused_y"] == 1 and sb["fused_y"] == 0
+    assert bool((a == b).all()), f"{name}: fused-y map differs from the three-operation form"
+    assert sa["sum_iters"] == sb["sum_iters"]

@@ -59,6 +59,7 @@ def main():
     global SCHEME
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C1")
+    ap.add_argument("--view", default="", help="xmin,xmax,ymin,ymax,W,H,iterMax (overrides --config's)")
     ap.add_argument("--kernels", default="lazy,refill")
     ap.add_argument("--tiles", default="0")
     ap.add_argument("--tile-rows", default="0")
@@ -73,6 +74,10 @@ def main():
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     base = wl.CONFIGS[a.config]
+    if a.view:
+        v = a.view.split(",")
+        base = base.with_(xmin=float(v[0]), xmax=float(v[1]), ymin=float(v[2]), ymax=float(v[3]),
+                          W=int(v[4]), H=int(v[5]), iter_max=int(v[6]))
     out = torch.zeros((base.H, base.W), dtype=torch.int32, device=dev)
     iters = [base.iter_max, 1] + [int(v) for v in a.iters.split(",") if v]
     for kern, tile, trows, ctas, lanes, minb in itertools.product(
@@ -80,7 +85,7 @@ def main():
             a.lanes.split(","), a.minb.split(",")):
         kw = dict(out_dev0=out, stream0=stream.cuda_stream, kernel=kern, tile_px=int(tile),
                   tile_rows=int(trows), ctas_per_sm=int(ctas), refill_lanes=int(lanes), min_ctas=int(minb))
-        rec = {"kernel": kern, "tile": int(tile), "tile_rows": int(trows), "ctas": int(ctas), "lanes": int(lanes),
+        rec = {"view": [base.xmin, base.xmax, base.ymin, base.ymax, base.W, base.H, base.iter_max], "kernel": kern, "tile": int(tile), "tile_rows": int(trows), "ctas": int(ctas), "lanes": int(lanes),
                "minb": int(minb)}
         try:
             st = mandel.mandel_render_ex(*base.args(), base.dtype, SCHEME, 1, **kw)

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--tile-rows", default="0", help="rows per tile, comma separated (0 = default)")
     ap.add_argument("--pack", default="1", help="fp32 packed batched loop: 1, 0 or 1,0")
     ap.add_argument("--stage", default="0", help="store staging: 1 staged, -1 direct, 0 default (comma list)")
+    ap.add_argument("--fused-y", default="0", help="options.fused_y (0 on, -1 off)")
     ap.add_argument("--ctas", default="0", help="resident CTAs per SM cap (0 = occupancy max), comma list")
     ap.add_argument("--chunks", default="16")
     ap.add_argument("--lanes", default="0", help="LAZY refill_lanes (0 = the library default, 16)")
@@ -64,7 +65,7 @@ def main():
                 continue
             kw = dict(out_dev0=out, stream0=stream.cuda_stream, kernel=kern,
                       tile_px=int(tile), tile_rows=int(trows), chunk_rows=int(chunk), refill_lanes=int(lanes),
-                      no_pack=pack == "0", stage=int(stage), ctas_per_sm=int(ctas),
+                      no_pack=pack == "0", stage=int(stage), ctas_per_sm=int(ctas), fused_y=int(a.fused_y),
                       min_ctas=int(minb) if kern != "static" else 0, adapt_lo=alo, adapt_hi=ahi)
             out.zero_()
             for _ in range(a.warmup):
@@ -89,7 +90,7 @@ def main():
             ops = 6 if cfg.dtype == "fp64fma" else 8
             peak = 148 * (128 if cfg.dtype == "fp32" else 64) * 1.965e9 / ops / 1e9
             print(json.dumps({"config": name, "dtype": cfg.dtype, "kernel": kern, "scheme": scheme, "tile": int(tile), "tile_rows": int(trows),
-                              "packed": st["kernel_packed"], "batch": st["kernel_batch"], "stage": int(stage), "ctas": int(ctas), "store": st["store_mode"],
+                              "packed": st["kernel_packed"], "batch": st["kernel_batch"], "stage": int(stage), "ctas": int(ctas), "store": st["store_mode"], "fused_y": st["fused_y"],
                               "chunk": int(chunk), "lanes": int(lanes), "minb": int(minb), "adapt": adapt, "ms": round(ms, 4),
                               "kernel_ms": round(sum(ks) / len(ks), 4),
                               "giter_s": round(giter, 2), "frac": round(giter / peak, 4),
