@@ -378,7 +378,16 @@ def run_ours(args):
             "kernel_ms_basis": kern_basis,
             "ops_per_launch": int(iters_launch * FLOPS_PER_ITER),
             "ops_per_launch_basis": f"{FLOPS_PER_ITER} FP ops (3 mul + 5 add/sub) x {iters_launch:.0f} "
-                                    "pixel-iterations (sum of this rank's counts) per launch"}
+                                    "pixel-iterations (sum of this rank's counts) per launch",
+            # the peak above is the FP pipe's lane-instruction rate (DADD/DMUL/DFMA: one each);
+            # the path executes fewer FP instructions than the 8 counted flops per iteration --
+            # the fused-y form does the *2 and +ci of Eq. 1's y-update in one FMA (R21)
+            # and the batched test forms |z|^2 once per 8 updates (R18) -- so frac can pass 1.
+            # Against the FMA flop peak (2 flops per lane-instruction) the same work is:
+            "peak_fma_flops": round(2 * peak, 4),
+            "frac_of_fma_flop_peak": round(achieved / (2 * peak), 4),
+            "executed_vs_counted": "fewer than 8 FP instructions per counted iteration (fused-y FMA; "
+                                   "batched |z|^2); ncu_pipe_active is the executed pipe utilisation"}
     prof = _traffic_from_profiles(cfg, world)
     if prof:
         # NOT measured in this run: read from the committed ncu --set full capture of this
@@ -589,7 +598,12 @@ def _traffic_from_profiles(cfg, world):
     capture summary (profiles/*_traffic.json), or None."""
     import glob
     best = None
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic*.json"))):
+
+    def round_tag(path):  # r01 < r01w < r02a < r02z < r02aa: newer tags are longer or later
+        tag = os.path.basename(path).split("_")[0]
+        return (len(tag), tag)
+
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic*.json")), key=round_tag):
         try:
             d = json.load(open(p))
         except (OSError, ValueError):
