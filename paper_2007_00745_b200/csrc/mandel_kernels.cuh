@@ -64,6 +64,14 @@ __device__ __forceinline__ void fcfs_delay(uint32_t salt, uint32_t odds_log2 = 1
 #endif
 }
 
+// A/B switches of the batch-start backup in the fused-y forms (ArithF64Y, ArithF32Y)
+#ifndef MANDEL_F64Y_SAVEX
+#define MANDEL_F64Y_SAVEX true
+#endif
+#ifndef MANDEL_F32Y_SAVEX
+#define MANDEL_F32Y_SAVEX true
+#endif
+
 #ifndef MANDEL_LAZY_UNROLL
 #define MANDEL_LAZY_UNROLL 16
 #endif
@@ -145,6 +153,8 @@ struct ArithF64 {
     typedef double T;
     typedef long long bits_t;
     static constexpr bool kPacked = false;
+    // the batched loop keeps the batch-start x as a copy (sx) instead of as x + x (t0)
+    static constexpr bool kSaveX = false;
     static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
     static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
     static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
@@ -223,6 +233,7 @@ struct ArithF32 {
     typedef float T;
     typedef int bits_t;
     static constexpr bool kPacked = false;
+    static constexpr bool kSaveX = false;
     static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
     static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
     static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
@@ -274,6 +285,10 @@ struct ArithF32 {
 // uses the same form (exact before the escape, so the recorded escape is the oracle's).
 // ---------------------------------------------------------------------------
 struct ArithF64Y : ArithF64 {
+    // x + x is no part of the fused update, so the batch start keeps a copy of x (two
+    // register moves, off the FP64 pipe) instead of computing x + x (one DADD per slot and
+    // batch on the pipe that bounds the loop)
+    static constexpr bool kSaveX = MANDEL_F64Y_SAVEX;
     static __device__ __forceinline__ void step(double& x, double& y, double& x2, double& y2,
                                                 double cr, double ci) {
         const double ny = __fma_rn(mul(x, y), 2.0, ci);
@@ -288,6 +303,9 @@ struct ArithF64Y : ArithF64 {
     }
 };
 struct ArithF32Y : ArithF32 {
+    // fp32 is issue-bound: a move costs the same issue slot as the x + x FADD, but not the
+    // FP32 pipe (C3 +0.4 %, profiles/r02al_c3_*.jsonl)
+    static constexpr bool kSaveX = MANDEL_F32Y_SAVEX;
     static __device__ __forceinline__ void step(float& x, float& y, float& x2, float& y2, float cr, float ci) {
         const float ny = __fmaf_rn(mul(x, y), 2.0f, ci);
         const float nx = add(sub(x2, y2), cr);
@@ -313,6 +331,7 @@ template <> struct FusedY<ArithF32> { typedef ArithF32Y type; static constexpr b
 // that ptxas cannot see through; the SASS gate test checks no FFMA2 remains.
 struct ArithF32P : ArithF32 {
     static constexpr bool kPacked = true;
+    static constexpr bool kSaveX = true;
     typedef unsigned long long u64;
     static __device__ __forceinline__ u64 pk(float a, float b) {
         u64 r;
@@ -790,7 +809,7 @@ __device__ __forceinline__ bool batch_key_hit(T (&x)[ILP], T (&y)[ILP], T (&x2)[
                                           uint32_t oz, const T (&t0)[ILP]) {
 #pragma unroll
     for (int u = 0; u < BT; ++u) {
-        if constexpr (!A::kPacked) {
+        if constexpr (!A::kSaveX) {
             if (u == 0) {  // the first update takes the caller's x + x (kept for the restore)
 #pragma unroll
                 for (int s = 0; s < ILP; ++s) A::step_t(t0[s], x[s], y[s], x2[s], y2[s], cr[s], ci[s]);
@@ -821,7 +840,7 @@ template <typename A, int ILP, int BT, int S, typename T, typename B>
 __device__ __forceinline__ void replay_slot(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
                                             const T (&cr)[ILP], const T (&ci)[ILP], const T (&t0)[ILP],
                                             const T (&sx)[ILP], const T (&sy)[ILP], B r2, uint32_t (&e)[ILP]) {
-    if constexpr (A::kPacked) x[S] = sx[S];
+    if constexpr (A::kSaveX) x[S] = sx[S];
     else x[S] = A::half(t0[S]);
     y[S] = sy[S];
     A::resq(x[S], y[S], x2[S], y2[S]);
@@ -877,7 +896,7 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                 for (;;) {
 #pragma unroll
                     for (int s = 0; s < ILP; ++s) {
-                        if constexpr (A::kPacked) sx[s] = x[s];
+                        if constexpr (A::kSaveX) sx[s] = x[s];
                         else t0[s] = A::add(x[s], x[s]);
                         sy[s] = y[s];
                     }
@@ -908,7 +927,7 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
                 } else {
 #pragma unroll
                     for (int s = 0; s < ILP; ++s) {
-                        if constexpr (A::kPacked) x[s] = sx[s];
+                        if constexpr (A::kSaveX) x[s] = sx[s];
                         else x[s] = A::half(t0[s]);  // (x + x) * 0.5 = x exactly
                         y[s] = sy[s];
                         A::resq(x[s], y[s], x2[s], y2[s]);
