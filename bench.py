@@ -398,6 +398,11 @@ def run_ours(args):
         pipe = prof.get("fp64_pipe_active_pct" if cfg.dtype != "fp32" else "fma_pipe_active_pct")
         if pipe is not None:
             roof["ncu_pipe_active"] = round(pipe / 100.0, 4)
+        # north_star's divergence evidence: active lanes per executed warp instruction
+        # (smsp__thread_inst_executed_per_inst_executed.ratio / 32); the static
+        # one-pixel-per-thread baseline beside it is in profiles/*_warp_efficiency.json
+        if prof.get("warp_execution_efficiency") is not None:
+            roof["ncu_warp_exec_eff"] = round(prof["warp_execution_efficiency"], 4)
         roof["ncu_kernel"] = prof.get("kernel")
         roof["traffic_source"] = (f"profiles/{os.path.basename(prof['_path'])}: committed ncu --set full "
                                   "capture of this kernel on this config (not measured in this run)")

@@ -296,13 +296,6 @@ KernelFn kernel_fn(int fp32, int variant, int ilp, int mi, int bt = 1) {
                                              MANDEL_BT_ROWS(ArithF64Fma, 4), MANDEL_BT_ROWS(ArithF32P, 4)};
         static const KernelFn b8[4][4][2] = {MANDEL_BT_ROWS(ArithF64, 8), MANDEL_BT_ROWS(ArithF32, 8),
                                              MANDEL_BT_ROWS(ArithF64Fma, 8), MANDEL_BT_ROWS(ArithF32P, 8)};
-        if (bt == 8 && kMinbVals[mi] == 4 && fp32 == 0 && ilp <= 2) {
-            // a 64-register budget (4 resident CTAs per SM) for the fp64 batched loop
-            // (options.min_ctas = 4 with check_every 8; DESIGN.md §6 occupancy)
-            static const KernelFn b8m4[2] = {escape_refill_kernel<ArithF64, 1, 4, 8>,
-                                             escape_refill_kernel<ArithF64, 2, 4, 8>};
-            return b8m4[ilp - 1];
-        }
         const int bi = kMinbVals[mi] == 1 ? 0 : (kMinbVals[mi] == 3 ? 1 : -1);
         if (bi < 0 || ilp < 1 || ilp > 4) return nullptr;
         static const KernelFn b16[2][4][2] = {MANDEL_BT_ROWS(ArithF64, 16), MANDEL_BT_ROWS(ArithF64Fma, 16)};
