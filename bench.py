@@ -44,6 +44,7 @@ import workloads as wl  # noqa: E402
 # lane per cycle (no FMA in this path, so ops = flops).
 SMS, FP64_LANES, FP32_LANES, SM_MAX_MHZ = 148, 64, 128, 1965.0
 FLOPS_PER_ITER = 8  # 3 mul + 5 add/sub per z-update
+MIN_FP_INSTR_PER_ITER = 6.125  # fused y (R21): 6 FP instructions per update + |z|^2 per 8 (R18)
 
 
 def fp_peak_tflops(dtype: str, mhz: float = SM_MAX_MHZ) -> float:
@@ -387,7 +388,12 @@ def run_ours(args):
             "peak_fma_flops": round(2 * peak, 4),
             "frac_of_fma_flop_peak": round(achieved / (2 * peak), 4),
             "executed_vs_counted": "fewer than 8 FP instructions per counted iteration (fused-y FMA; "
-                                   "batched |z|^2); ncu_pipe_active is the executed pipe utilisation"}
+                                   "batched |z|^2); ncu_pipe_active is the executed pipe utilisation",
+            # the same time against the fewest FP instructions an exact evaluation needs per
+            # iteration -- 6 per z-update in the fused form (x*x, y*y, x*y, -, +cr, fma) and the
+            # |z|^2 add once per 8 updates (R18) -- so this fraction cannot pass 1
+            "frac_min_fp_instr": round(iters_launch * MIN_FP_INSTR_PER_ITER / (kern_ms * 1e-3) / 1e12 / peak, 4),
+            "min_fp_instr_per_iter": MIN_FP_INSTR_PER_ITER}
     prof = _traffic_from_profiles(cfg, world)
     if prof:
         # NOT measured in this run: read from the committed ncu --set full capture of this

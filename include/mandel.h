@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 8
+#define MANDEL_ABI_VERSION 9
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -139,6 +139,9 @@ typedef struct mandel_stats {
                                       the tile width multiples of 4)                               */
     int32_t  fused_y;              /* 1: the fused-y form was enabled for rank 0's launch (its warps
                                       use it where their pixels allow, options.fused_y)         */
+    int32_t  host_handoff;         /* 1: the per-device host hand-off ran (options.host_handoff):
+                                      d2h_ms is then from the last kernel's end to the last rank's
+                                      last copy, and transfers counts the device->host copies     */
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
@@ -204,6 +207,15 @@ typedef struct mandel_options {
                                 same rounded value, one instruction fewer per update; other
                                 warps and views use the three-operation form.  -1 -> always the
                                 three-operation form.  Counts are identical either way.        */
+    int      host_handoff;   /* mandel_render / _ex with out_host and ngpus > 1: how the map reaches
+                                the host.  -1 -> through GPU 0: every rank stores into GPU 0's map
+                                (the fused gather) and GPU 0 copies W*H*4 bytes to out_host;
+                                1 -> per device: every rank stores its rows into a band in its own
+                                device memory and its device copies them to their rows of
+                                out_host (N links in parallel, each copy starting when its rank's
+                                kernel ends; FCFS: after reading back the rank's chunk map);
+                                0 -> default: per device when the ranks span more than one GPU.
+                                Ignored with one rank or without out_host.                      */
 } mandel_options;
 
 /*

@@ -181,6 +181,11 @@ struct RankCtx {
     int par = 0;
     size_t zeroed[2] = {0, 0};  // bytes of each half known to be zero
     void* half(int k) const { return static_cast<char*>(state) + (size_t)k * state_bytes; }
+    // the per-device host hand-off (options.host_handoff): this rank's rows, stored on its
+    // own device and copied to the host over its own link
+    uint32_t* band = nullptr;
+    size_t band_bytes = 0;
+    cudaEvent_t d2h = nullptr;
 };
 
 constexpr int kMaxBands = 32;
@@ -396,7 +401,9 @@ int ensure_rank(int r, int dev, size_t state_bytes, cudaStream_t user_stream) {
             if (rc.k0) cudaEventDestroy(rc.k0);
             if (rc.k1) cudaEventDestroy(rc.k1);
             if (rc.used) cudaEventDestroy(rc.used);
+            if (rc.d2h) cudaEventDestroy(rc.d2h);
             if (rc.state) cudaFree(rc.state);
+            if (rc.band) cudaFree(rc.band);
             rc = RankCtx();
         }
         rc.device = dev;
@@ -1078,6 +1085,66 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
     return MANDEL_OK;
 }
 
+// The per-device host hand-off (options.host_handoff): enqueue, on every rank's stream
+// after its kernel, the copies of its band's rows into their image rows of out_host, and
+// record the rank's d2h event after them.  Static schemes: the plan is known before the
+// kernel runs -- slots [0, count0) are rows base0 + s * stride0 (one strided 2-D copy),
+// slots [count0, nslots) rows base1 + ... (one contiguous copy).  FCFS: local chunk k
+// holds global chunk chunk_map[k] - 1 (bound in local order; 0 / kChunkDone end the
+// list), read back once the rank's kernel is done; runs of consecutive global chunks are
+// copied as one block of rows.  copies counts the copies enqueued.
+int copy_bands_to_host(const std::vector<LaunchSpec>& specs, int ngpus, cudaStream_t s0, uint32_t W,
+                       uint32_t H, uint32_t* out_host, uint32_t& copies) {
+    const size_t row_bytes = (size_t)W * sizeof(uint32_t);
+    std::vector<std::vector<uint32_t>> cmap(ngpus);
+    // FCFS chunk maps first, so that each rank's read waits only for its own kernel
+    for (int r = 0; r < ngpus; ++r) {
+        const mandel::Params& p = specs[r].p;
+        if (p.scheme != MANDEL_FCFS) continue;
+        RankCtx& rk = g_rank[r];
+        CK(cudaSetDevice(rk.device));
+        cmap[r].resize((size_t)p.nchunks + 1);
+        CK(cudaMemcpyAsync(cmap[r].data(), p.chunk_map, cmap[r].size() * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, r == 0 ? s0 : rk.stream));
+    }
+    for (int r = 0; r < ngpus; ++r) {
+        const mandel::Params& p = specs[r].p;
+        RankCtx& rk = g_rank[r];
+        cudaStream_t s = r == 0 ? s0 : rk.stream;
+        CK(cudaSetDevice(rk.device));
+        if (p.scheme == MANDEL_FCFS) {
+            CK(cudaStreamSynchronize(s));
+            const uint32_t c = p.chunk_rows;
+            uint32_t k = 0;
+            while (k <= p.nchunks) {
+                const uint32_t g = cmap[r][k];
+                if (g == 0 || g == mandel::kChunkDone) break;
+                uint32_t n = 1;  // a run of local chunks bound to consecutive global chunks
+                while (k + n <= p.nchunks && cmap[r][k + n] == g + n) ++n;
+                const uint64_t row0 = (uint64_t)(g - 1) * c;
+                const uint64_t rows = std::min<uint64_t>((uint64_t)n * c, H - row0);
+                CK(cudaMemcpyAsync(out_host + row0 * W, p.out + (size_t)k * c * W, rows * row_bytes,
+                                   cudaMemcpyDeviceToHost, s));
+                ++copies;
+                k += n;
+            }
+        } else {
+            if (p.count0 > 0) {
+                CK(cudaMemcpy2DAsync(out_host + (size_t)p.base0 * W, (size_t)p.stride0 * row_bytes, p.out,
+                                     row_bytes, row_bytes, p.count0, cudaMemcpyDeviceToHost, s));
+                ++copies;
+            }
+            if (p.nslots > p.count0) {
+                CK(cudaMemcpyAsync(out_host + (size_t)p.base1 * W, p.out + (size_t)p.count0 * W,
+                                   (size_t)(p.nslots - p.count0) * row_bytes, cudaMemcpyDeviceToHost, s));
+                ++copies;
+            }
+        }
+        CK(cudaEventRecord(rk.d2h, s));
+    }
+    return MANDEL_OK;
+}
+
 int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, uint32_t H,
                 uint32_t iter_max, double R, int dtype, int scheme, int ngpus,
                 const mandel_options* opts, uint32_t* out_host, uint32_t* out_dev0,
@@ -1174,6 +1241,21 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         if (rc == MANDEL_OK && cms > 0) g_view_ms[vkey] = cms;
         return rc;
     }
+    // Host hand-off of a multi-rank render (options.host_handoff).  Through GPU 0: every
+    // rank stores into GPU 0's map (the fused gather) and GPU 0 copies W*H*4 bytes to the
+    // host over its one link.  Per device (the default when the ranks span several GPUs):
+    // every rank stores its rows into a band in its own HBM (band mode, local stores) and
+    // its own device copies them into out_host -- the copies of N GPUs run over N links
+    // and each starts when its rank's kernel ends (PAPER.md:151 sends each task's rows to
+    // the master; here the host is the master).
+    const int hh = opts ? opts->host_handoff : 0;
+    if (hh < -1 || hh > 1) return fail(MANDEL_EINVAL, "options.host_handoff must be -1, 0 or 1");
+    const bool per_dev = out_host && !out_dev0 && (hh == 1 || (hh == 0 && nphys > 1));
+    mandel_options bopt;
+    if (opts) bopt = *opts;
+    else std::memset(&bopt, 0, sizeof(bopt));
+    bopt.band_out = 1;
+    const mandel_options* ropts = per_dev ? &bopt : opts;
     std::vector<LaunchSpec> specs(ngpus);
     const int cp = g_root.ctr_par;  // the counter word this render claims from
     for (int r = 0; r < ngpus; ++r) {
@@ -1181,10 +1263,27 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         rc = ensure_rank(r, dev, sbytes, nullptr);
         if (rc) return rc;
         RankCtx& rk = g_rank[r];
-        rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, opts, image, rk.half(rk.par),
-                          rk.state_bytes, g_root.fcfs_ctr + 32 * cp, nphys > 1, dev, specs[r], nullptr, kcp,
-                          dev != 0);
+        rc = build_params(d, W, H, iter_max, dtype, scheme, ngpus, r, ropts, per_dev ? nullptr : image,
+                          rk.half(rk.par), rk.state_bytes, g_root.fcfs_ctr + 32 * cp, nphys > 1, dev, specs[r],
+                          nullptr, kcp, !per_dev && dev != 0);
         if (rc) return rc;
+        if (per_dev) {
+            // the band holds the rank's row slots: static schemes the plan's rows, FCFS up to
+            // every chunk (band row k * chunk_rows + r = local chunk k, row r)
+            const mandel::Params& p = specs[r].p;
+            const uint64_t rows = p.scheme == MANDEL_FCFS ? (uint64_t)p.nchunks * p.chunk_rows : p.nslots;
+            const size_t need = std::max<size_t>((size_t)(rows * W * sizeof(uint32_t)), 256);
+            if (rk.band_bytes < need) {
+                CK(cudaEventSynchronize(rk.used));  // an earlier render may still copy from it
+                if (rk.band) CK(cudaFree(rk.band));
+                rk.band = nullptr;
+                rk.band_bytes = 0;
+                CK(cudaMalloc(&rk.band, need));
+                rk.band_bytes = need;
+            }
+            if (!rk.d2h) CK(cudaEventCreateWithFlags(&rk.d2h, cudaEventDisableTiming));
+            specs[r].p.out = rk.band;
+        }
         // the kernel zeroes the rank's other half (and rank 0 the other counter word) for the
         // next render
         specs[r].p.zero_next = static_cast<uint32_t*>(rk.half(rk.par ^ 1));
@@ -1228,6 +1327,16 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     CK(cudaSetDevice(0));
     for (int r = 1; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].k1, 0));
     if (timed) CK(cudaEventRecord(g_root.done, s0));
+    uint32_t d2h_copies = 0;
+    if (per_dev) {
+        // each rank's copies follow its own kernel on its own stream (rank 0's follow the
+        // done event on s0, so device_ms stays the compute); the map is complete on the
+        // host once GPU 0's stream has waited for every rank's last copy
+        rc = copy_bands_to_host(specs, ngpus, s0, W, H, out_host, d2h_copies);
+        if (rc) return rc;
+        CK(cudaSetDevice(0));
+        for (int r = 0; r < ngpus; ++r) CK(cudaStreamWaitEvent(s0, g_rank[r].d2h, 0));
+    }
     // every rank's state and the counter are free once GPU 0's stream passes here
     for (int r = 0; r < ngpus; ++r) {
         CK(cudaSetDevice(g_rank[r].device));
@@ -1237,7 +1346,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
     // device output without statistics: enqueued only (stream0 orders everything after it)
     if (!stats && !out_host) return MANDEL_OK;
     if (out_host) {
-        CK(cudaMemcpyAsync(out_host, image, bytes, cudaMemcpyDeviceToHost, s0));
+        if (!per_dev) CK(cudaMemcpyAsync(out_host, image, bytes, cudaMemcpyDeviceToHost, s0));
         CK(cudaEventRecord(g_root.d2h, s0));
     }
     // read back per-rank statistics (small, ordered after each rank's kernel)
@@ -1286,7 +1395,9 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         stats->chunks_claimed = claims;
         stats->kernel_scheme = scheme;
         stats->sm_clock_mhz = clock_mhz(ws.data(), ngpus);
-        stats->transfers = transfers;
+        // per-device hand-off: no gather to rank 0; the transfers are the copies to the host
+        stats->transfers = per_dev ? d2h_copies : transfers;
+        stats->host_handoff = per_dev ? 1 : 0;
         stats->kernel_launches = (uint32_t)launches;
         stats->ngpus = (uint32_t)ngpus;
         stats->ndevices = (uint32_t)nphys;
@@ -1681,7 +1792,12 @@ void mandel_shutdown(void) {
             cudaEventSynchronize(rc.used);
             cudaEventDestroy(rc.used);
         }
+        if (rc.d2h) {
+            cudaEventSynchronize(rc.d2h);
+            cudaEventDestroy(rc.d2h);
+        }
         if (rc.state) cudaFree(rc.state);
+        if (rc.band) cudaFree(rc.band);
         rc = RankCtx();
     }
     if (!g_dev.empty()) {

@@ -80,6 +80,7 @@ class mandel_stats(ctypes.Structure):
         ("kernel_scheme", ctypes.c_int32),
         ("store_mode", ctypes.c_int32),
         ("fused_y", ctypes.c_int32),
+        ("host_handoff", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -101,6 +102,7 @@ class mandel_stats(ctypes.Structure):
             "kernel_batch": int(self.kernel_batch), "kernel_packed": int(self.kernel_packed),
             "sm_clock_mhz": float(self.sm_clock_mhz),
             "fused_y": int(self.fused_y),
+            "host_handoff": "per_device" if int(self.host_handoff) else "gpu0",
             "store_mode": {0: "direct", 1: "staged", 2: "staged_vec"}.get(int(self.store_mode), str(self.store_mode)),
             "kernel_scheme": {v: k for k, v in SCHEMES.items() if k not in ("naive", "alternating")}.get(
                 int(self.kernel_scheme), str(self.kernel_scheme)),
@@ -129,6 +131,7 @@ class mandel_options(ctypes.Structure):
         ("stage", ctypes.c_int),
         ("ctas_per_sm", ctypes.c_int),
         ("fused_y", ctypes.c_int),
+        ("host_handoff", ctypes.c_int),
     ]
 
 
@@ -255,7 +258,7 @@ def _buf(a, nbytes: int, name: str) -> int | None:
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
           tile_rows=0, no_pack=False, band_out=False, band_taper=0, max_sms=0, async_host=False,
-          stage=0, ctas_per_sm=0, fused_y=0):
+          stage=0, ctas_per_sm=0, fused_y=0, host_handoff=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -278,6 +281,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.stage = int(stage)
     o.ctas_per_sm = int(ctas_per_sm)
     o.fused_y = int(fused_y)
+    o.host_handoff = int(host_handoff)
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -309,7 +313,8 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
                      bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0,
-                     max_sms=0, async_host=False, stage=0, ctas_per_sm=0, fused_y=0, want_stats=True):
+                     max_sms=0, async_host=False, stage=0, ctas_per_sm=0, fused_y=0, host_handoff=0,
+                     want_stats=True):
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict; want_stats=False (device output only)
@@ -321,7 +326,7 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
               refill_lanes=refill_lanes, ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo,
               adapt_hi=adapt_hi, bands=bands, check_every=check_every, tile_rows=tile_rows,
               no_pack=no_pack, band_taper=band_taper, max_sms=max_sms, async_host=async_host,
-              stage=stage, ctas_per_sm=ctas_per_sm, fused_y=fused_y)
+              stage=stage, ctas_per_sm=ctas_per_sm, fused_y=fused_y, host_handoff=host_handoff)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), host_p,
                                 dev_p, stream0, ctypes.byref(st) if st is not None else None)

@@ -42,6 +42,9 @@ def _check_contract(d, n_gpus):
     # profile-derived fields labelled, the in-kernel SM clock, a single-render latency
     assert r["peak_basis"].startswith("measured") and r["peak_unit_count"] > 0
     assert abs(r["frac_unit_count"] - r["achieved"] / r["peak_unit_count"]) < 1e-3
+    # against the fewest FP instructions an exact evaluation needs, the fraction is a real one
+    assert 0 < r["frac_min_fp_instr"] <= 1.0, r
+    assert abs(r["frac_min_fp_instr"] - r["frac"] * r["min_fp_instr_per_iter"] / 8) < 2e-3
     if r.get("traffic") is not None:
         assert "not measured in this run" in r["traffic_source"]
     assert 500 < c["sm_mhz_in_kernel"] < 2500, c

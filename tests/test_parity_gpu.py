@@ -827,3 +827,62 @@ def test_fused_y_whole_map_matches_exact_form(mandel, name):
     assert sa["fused_y"] == 1 and sb["fused_y"] == 0
     assert bool((a == b).all()), f"{name}: fused-y map differs from the three-operation form"
     assert sa["sum_iters"] == sb["sum_iters"]
+
+
+# ---------------------------------------------------------------------------
+# per-device host hand-off (options.host_handoff = 1): every rank's band copied to the
+# host by its own device -- forced here, where all logical ranks share cuda:0
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme", ["block", "cyclic", "fcfs", "fcfs_master"])
+@pytest.mark.parametrize("ngpus", [2, 3, 5, 8])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_host_handoff_per_device(mandel, oracle, dtype, scheme, ngpus):
+    cfg = wl.C1.with_(dtype=dtype, W=517, H=389)  # ragged: H not a multiple of the chunk or N
+    want = oracle.render(cfg)
+    got = np.full((cfg.H, cfg.W), 0xDEADBEEF, np.uint32)
+    kw = dict(chunk_rows=[0, 5, 16, 1][ngpus % 4]) if scheme == "fcfs" else {}
+    st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, ngpus, out_host=got, logical_ranks=True,
+                                 host_handoff=1, **kw)
+    _assert_same(got, want, f"per-device hand-off {dtype}/{scheme}/N={ngpus}")
+    assert st["host_handoff"] == "per_device"
+    assert st["sum_iters"] == int(want.sum(dtype=np.uint64)) and st["pixels"] == cfg.pixels
+    assert st["transfers"] >= 1 and st["d2h_ms"] >= 0
+    if scheme in ("block", "cyclic"):
+        # static plans: one (strided) copy per rank plus the cyclic tail on rank 0
+        plans = [mandel.mandel_plan_rows(scheme, cfg.H, ngpus, r) for r in range(ngpus)]
+        assert ngpus <= st["transfers"] <= ngpus + 1, (st["transfers"], [len(p) for p in plans])
+    # the default with one device is the gather through GPU 0; a repeated call reuses the bands
+    got2 = np.zeros_like(got)
+    st2 = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, ngpus, out_host=got2, logical_ranks=True,
+                                  **kw)
+    _assert_same(got2, want, "through GPU 0")
+    assert st2["host_handoff"] == "gpu0"
+    got3 = np.zeros_like(got)
+    mandel.mandel_render_ex(*cfg.args(), cfg.dtype, scheme, ngpus, out_host=got3, logical_ranks=True,
+                            host_handoff=1, **kw)
+    _assert_same(got3, want, "per-device hand-off, second call")
+
+
+def test_host_handoff_rejects_bad_value(mandel):
+    cfg = wl.C1.with_(W=32, H=32)
+    o = np.zeros((cfg.H, cfg.W), np.uint32)
+    for v in (-2, 2):
+        with pytest.raises(mandel.MandelError):
+            mandel.mandel_render_ex(*cfg.args(), "fp64", "block", 2, out_host=o, logical_ranks=True,
+                                    host_handoff=v)
+
+
+def test_host_handoff_large_pinned(mandel, oracle):
+    """C2-shaped map through the per-device hand-off into pinned memory: sampled rows
+    against the oracle, Σcounts against the map."""
+    torch = _torch()
+    cfg = wl.C2
+    host = torch.zeros((cfg.H, cfg.W), dtype=torch.int32, pin_memory=True)
+    st = mandel.mandel_render_ex(*cfg.args(), cfg.dtype, "fcfs", 4, out_host=host, logical_ranks=True,
+                                 host_handoff=1)
+    m = host.numpy().view(np.uint32)
+    assert st["host_handoff"] == "per_device"
+    assert int(m.sum(dtype=np.uint64)) == st["sum_iters"] and m.min() >= 1
+    rows = np.sort(np.random.default_rng(7).choice(cfg.H, 24, replace=False))
+    want, _ = oracle.render_rows_mt(cfg, rows)
+    _assert_same(m[rows], want, "C2 per-device hand-off rows")
