@@ -92,7 +92,18 @@ def main():
                    chunk_rows=int(rng.choice([0, 1, 3, 16])))
         hscheme = ["block", "cyclic", "fcfs"][n_cfg % 3]
         try:
-            if n_cfg % 2:  # asynchronous pipelined host output (finished right away)
+            if n_cfg % 5 == 0:  # several logical ranks, the per-device host hand-off (bands)
+                nr = int(rng.choice([2, 3, 5, 8]))
+                hs = hscheme if rng.random() < 0.8 else "fcfs_master"
+                if hs in ("block", "cyclic") and cfg.H < nr:
+                    nr = 2 if cfg.H >= 2 else 1
+                got = np.zeros((cfg.H, cfg.W), np.uint32)
+                hkw = dict(chunk_rows=hkw["chunk_rows"], tile_rows=hkw["tile_rows"], tile_px=hkw["tile_px"],
+                           host_handoff=1, ngpus=nr, scheme=hs)
+                mandel.mandel_render_ex(*cfg.args(), dtype, hs, nr, out_host=got, logical_ranks=True,
+                                        host_handoff=1, chunk_rows=hkw["chunk_rows"], tile_rows=hkw["tile_rows"],
+                                        tile_px=hkw["tile_px"])
+            elif n_cfg % 2:  # asynchronous pipelined host output (finished right away)
                 got = np.zeros((cfg.H, cfg.W), np.uint32)
                 mandel.mandel_render_ex(*cfg.args(), dtype, hscheme, 1, out_host=got, async_host=True,
                                         want_stats=False, **hkw)
