@@ -447,6 +447,7 @@ def run_ours(args):
             "kernel_scheme": stats[-1].get("kernel_scheme"),
             "chunks_claimed_per_step": sum_over_ranks(dist, [stats[-1]["chunks_claimed"]], adev)[0],
             "kernel_variant": stats[-1].get("kernel"),
+            "first_block_lanes": stats[-1].get("first_block"),
             "parallelism": f"{args.scheme} rows over {world} GPU(s)",
             "gather": "none (1 GPU)" if world == 1 else (
                 "fused: every rank's kernel stores into rank 0's map over NVLink (CUDA IPC)"

@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define MANDEL_ABI_VERSION 9
+#define MANDEL_ABI_VERSION 10
 #define MANDEL_MAX_GPUS 64          /* logical ranks (physical GPUs <= device count) */
 #define MANDEL_IPC_HANDLE_BYTES 64  /* size of a cudaIpcMemHandle_t                  */
 
@@ -142,6 +142,9 @@ typedef struct mandel_stats {
     int32_t  host_handoff;         /* 1: the per-device host hand-off ran (options.host_handoff):
                                       d2h_ms is then from the last kernel's end to the last rank's
                                       last copy, and transfers counts the device->host copies     */
+    int32_t  first_block;          /* lanes' worth of fresh slots that start an exactly recorded first
+                                      block in rank 0's launch (options.first_block); 0: none (the
+                                      kernel is not a batched EAGER one, or -1 was asked)          */
 } mandel_stats;
 
 /* Optional knobs for mandel_render_ex / mandel_render_rank (NULL = defaults). */
@@ -216,6 +219,14 @@ typedef struct mandel_options {
                                 kernel ends; FCFS: after reading back the rank's chunk map);
                                 0 -> default: per device when the ranks span more than one GPU.
                                 Ignored with one rank or without out_host.                      */
+    int      first_block;    /* EAGER batched kernels (check_every > 1): a refill that hands fresh
+                                pixels to at least this many lanes' worth of the warp's slots
+                                (1..32) starts with one block of 8 z-updates whose Eq. 2 test is
+                                recorded exactly after every update (as the LAZY kernel does)
+                                instead of a batch that would hit and be replayed -- the warp is
+                                in the exterior, where counts are a few updates.  Counts are
+                                identical either way.  0 -> default
+                                (16); -1 -> never; otherwise MANDEL_EINVAL                        */
 } mandel_options;
 
 /*

@@ -351,6 +351,7 @@ struct KernelChoice {
 constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 3, 8, 0, 0},    // fp64
                                             {MANDEL_KERNEL_EAGER, 1, 3, 8, 0, 4},    // fp32
                                             {MANDEL_KERNEL_EAGER, 2, 3, 8, 0, 0}};   // fp64 FMA
+constexpr uint32_t kDefaultFirstBlock = 16;   // options.first_block
 constexpr uint32_t kDefaultRefillLanes = 16;  // LAZY on C4: 8 -> 1509, 16 -> 1555 Giter/s
 constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
 constexpr double kDefaultBandTaper = 0.7;  // band pair p holds a 0.7^p share of the rows
@@ -629,6 +630,11 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
                                     : (kc.lanes ? kc.lanes : (int)kDefaultRefillLanes);
     if (rl < 1 || rl > 32) return fail(MANDEL_EINVAL, "options.refill_lanes must be in 1..32");
     p.refill_lanes = (uint32_t)rl;
+    // first block (mandel_kernels.cuh): lanes' worth of fresh slots
+    // that start one (C2: off 5.17, 8 -> 5.01, 16 -> 5.03, 32 -> 5.06 ms; profiles/r02ar_*)
+    const int fb = o ? o->first_block : 0;
+    if (fb < -1 || fb > 32) return fail(MANDEL_EINVAL, "options.first_block must be -1 or in 0..32");
+    p.first_block = fb < 0 ? 0xffffffffu : (uint32_t)((fb ? fb : (int)kDefaultFirstBlock) * kc.ilp);
     p.adapt_lo = (o && o->adapt_lo > 0) ? (uint32_t)o->adapt_lo : kDefaultAdaptLo;
     p.adapt_hi = (o && o->adapt_hi > 0) ? (uint32_t)o->adapt_hi : kDefaultAdaptHi;
     ls.block = persistent ? dim3(mandel::kCtaThreads) : dim3(32, mandel::kWarpsPerCta);
@@ -669,6 +675,12 @@ bool same_device(const void* ptr, int dev) {
 }
 
 int store_mode(const mandel::Params& p) { return p.stage ? (p.vec_ok ? 2 : 1) : 0; }
+
+// mandel_stats.first_block: the threshold in lanes, 0 when the launch runs no first block
+int first_block_lanes(const LaunchSpec& ls) {
+    const bool on = ls.kc.variant == MANDEL_KERNEL_EAGER && ls.kc.bt > 1 && ls.p.first_block != 0xffffffffu;
+    return on ? (int)(ls.p.first_block / (uint32_t)std::max(ls.kc.ilp, 1)) : 0;
+}
 
 // SM clock over a set of kernel states (mandel_stats.sm_clock_mhz): sum of cycles / sum of ns
 double clock_mhz(const mandel::WorkState* ws, int n) {
@@ -1078,6 +1090,7 @@ int render_banded(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, i
         stats->kernel_packed = specs[0].kc.packed;
         stats->store_mode = store_mode(specs[0].p);
         stats->fused_y = (int32_t)specs[0].p.fused_y;
+        stats->first_block = first_block_lanes(specs[0]);
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -1407,6 +1420,7 @@ int render_impl(double xmin, double xmax, double ymin, double ymax, uint32_t W, 
         stats->kernel_packed = specs[0].kc.packed;
         stats->store_mode = store_mode(specs[0].p);
         stats->fused_y = (int32_t)specs[0].p.fused_y;
+        stats->first_block = first_block_lanes(specs[0]);
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t_call;
@@ -1614,6 +1628,7 @@ int mandel_render_rank(double xmin, double xmax, double ymin, double ymax, uint3
         stats->kernel_packed = ls.kc.packed;
         stats->store_mode = store_mode(ls.p);
         stats->fused_y = (int32_t)ls.p.fused_y;
+        stats->first_block = first_block_lanes(ls);
         stats->probe[0] = g_probe[0];
         stats->probe[1] = g_probe[1];
         stats->total_ms = now_ms() - t0;

@@ -133,6 +133,8 @@ struct Params {
     uint32_t claim_batch;            // FCFS: chunks per claim (1 when ranks compete; more for one)
     uint32_t fcfs_sys;               // 1: the counter is shared across devices (system-scope atomics)
     uint32_t refill_lanes;           // lazy refill: leave the loop when this many lanes are free
+    uint32_t first_block;            // EAGER batched: a refill of at least this many slots starts with
+                                     // one exactly recorded block (0: never)
     uint32_t adapt_lo, adapt_hi;     // adaptive: eager->lazy below adapt_lo iterations per run,
                                      // lazy->eager above adapt_hi
     uint32_t* out;                   // rank 0's image, row-major W per row (local or peer)
@@ -1014,6 +1016,15 @@ __device__ __forceinline__ uint32_t eager_run(const Params& p, T (&x)[ILP], T (&
 // the two counters cost ~3% on C2 in production, measured A/B).
 // STAGE: stores go through the per-warp staging ring (the instantiation the host picks
 // when p.stage is set; without it the kernel keeps no staging state at all).
+#ifndef MANDEL_FIRST_BLOCK
+#define MANDEL_FIRST_BLOCK 8
+#endif
+constexpr int kFirstBlock = MANDEL_FIRST_BLOCK;  // updates of the first block after a large refill
+template <typename AR, int ILP, int LU, typename T>
+__device__ __forceinline__ void lazy_block(T (&x)[ILP], T (&y)[ILP], T (&x2)[ILP], T (&y2)[ILP],
+                                           const T (&cr)[ILP], const T (&ci)[ILP],
+                                           typename AR::bits_t r2, uint32_t (&e)[ILP]);
+
 template <typename AR, int ILP, int MINB, int BT = 1, bool LSTATS = false, bool STAGE = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB)
 escape_refill_kernel(const Params p) {
@@ -1146,8 +1157,27 @@ escape_refill_kernel(const Params p) {
             for (int s = 0; s < ILP; ++s) ok = ok && fs[s];
             fast = __all_sync(FULL, ok);
         }
-        const uint32_t k = fast ? eager_run<AF, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax)
-                                : eager_run<A, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax);
+        uint32_t k;
+        if (BT > 1 && !LSTATS && nd >= p.first_block && kmax >= (uint32_t)kFirstBlock) {
+            // ---- first block: a refill that handed out many fresh pixels (the warp is in the
+            // exterior, where counts are a few updates) runs kFirstBlock updates with the exact
+            // Eq. 2 test recorded after each (lazy_block) instead of a batch that would hit and
+            // be replayed: half the updates per escape there.  Slots that did not escape keep
+            // their exact state and go on in the batched loop.
+            uint32_t e[ILP];
+            const typename A::bits_t r2 = (typename A::bits_t)p.r2bits;
+            if (fast) lazy_block<AF, ILP, kFirstBlock>(x, y, x2, y2, cr, ci, r2, e);
+            else lazy_block<A, ILP, kFirstBlock>(x, y, x2, y2, cr, ci, r2, e);
+#pragma unroll
+            for (int s = 0; s < ILP; ++s) {
+                fin[s] = rem[s] != kIdleRem && e[s] < (uint32_t)kFirstBlock;  // R3: count the escaping update
+                kx[s] = fin[s] ? e[s] + 1u : (uint32_t)kFirstBlock;
+            }
+            k = kFirstBlock;
+        } else {
+            k = fast ? eager_run<AF, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax)
+                     : eager_run<A, ILP, BT>(p, x, y, x2, y2, cr, ci, rem, fin, kx, kmax);
+        }
 
         if (LSTATS) {
             w_iters += k;

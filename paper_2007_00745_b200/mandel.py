@@ -81,6 +81,7 @@ class mandel_stats(ctypes.Structure):
         ("store_mode", ctypes.c_int32),
         ("fused_y", ctypes.c_int32),
         ("host_handoff", ctypes.c_int32),
+        ("first_block", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -102,6 +103,7 @@ class mandel_stats(ctypes.Structure):
             "kernel_batch": int(self.kernel_batch), "kernel_packed": int(self.kernel_packed),
             "sm_clock_mhz": float(self.sm_clock_mhz),
             "fused_y": int(self.fused_y),
+            "first_block": int(self.first_block),
             "host_handoff": "per_device" if int(self.host_handoff) else "gpu0",
             "store_mode": {0: "direct", 1: "staged", 2: "staged_vec"}.get(int(self.store_mode), str(self.store_mode)),
             "kernel_scheme": {v: k for k, v in SCHEMES.items() if k not in ("naive", "alternating")}.get(
@@ -132,6 +134,7 @@ class mandel_options(ctypes.Structure):
         ("ctas_per_sm", ctypes.c_int),
         ("fused_y", ctypes.c_int),
         ("host_handoff", ctypes.c_int),
+        ("first_block", ctypes.c_int),
     ]
 
 
@@ -258,7 +261,7 @@ def _buf(a, nbytes: int, name: str) -> int | None:
 def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=False,
           refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0, bands=0, check_every=0,
           tile_rows=0, no_pack=False, band_out=False, band_taper=0, max_sms=0, async_host=False,
-          stage=0, ctas_per_sm=0, fused_y=0, host_handoff=0):
+          stage=0, ctas_per_sm=0, fused_y=0, host_handoff=0, first_block=0):
     """kernel: a mandel_kernel value or a KERNELS name (which may also fix ilp)."""
     o = mandel_options()
     if isinstance(kernel, str):
@@ -282,6 +285,7 @@ def _opts(chunk_rows=0, tile_px=0, kernel=MANDEL_KERNEL_REFILL, logical_ranks=Fa
     o.ctas_per_sm = int(ctas_per_sm)
     o.fused_y = int(fused_y)
     o.host_handoff = int(host_handoff)
+    o.first_block = int(first_block)
     o.chunk_rows = chunk_rows or 0
     o.tile_px = tile_px or 0
     o.kernel = kernel
@@ -314,7 +318,7 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
                      refill_lanes=0, ilp=0, min_ctas=0, adapt_lo=0, adapt_hi=0,
                      bands=0, check_every=0, tile_rows=0, no_pack=False, band_taper=0,
                      max_sms=0, async_host=False, stage=0, ctas_per_sm=0, fused_y=0, host_handoff=0,
-                     want_stats=True):
+                     first_block=0, want_stats=True):
     """C: mandel_render_ex.  out_host: numpy/pinned tensor; out_dev0: CUDA tensor or
     device pointer on device 0; stream0: cudaStream_t handle (int) on device 0.
     Returns the call's statistics as a dict; want_stats=False (device output only)
@@ -326,7 +330,8 @@ def mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype="fp64", sc
               refill_lanes=refill_lanes, ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo,
               adapt_hi=adapt_hi, bands=bands, check_every=check_every, tile_rows=tile_rows,
               no_pack=no_pack, band_taper=band_taper, max_sms=max_sms, async_host=async_host,
-              stage=stage, ctas_per_sm=ctas_per_sm, fused_y=fused_y, host_handoff=host_handoff)
+              stage=stage, ctas_per_sm=ctas_per_sm, fused_y=fused_y, host_handoff=host_handoff,
+              first_block=first_block)
     rc = lib().mandel_render_ex(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                 _enum(scheme, SCHEMES), ngpus, ctypes.byref(o), host_p,
                                 dev_p, stream0, ctypes.byref(st) if st is not None else None)
@@ -338,7 +343,8 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
                        out_root, fcfs_counter=None, stream=None, chunk_rows=0, tile_px=0,
                        kernel=MANDEL_KERNEL_REFILL, refill_lanes=0, ilp=0,
                        min_ctas=0, adapt_lo=0, adapt_hi=0, check_every=0, tile_rows=0,
-                       no_pack=False, band_out=False, max_sms=0, stage=0, fused_y=0, want_stats=True):
+                       no_pack=False, band_out=False, max_sms=0, stage=0, fused_y=0, first_block=0,
+                       want_stats=True):
     """C: mandel_render_rank (one process per GPU).  out_root / fcfs_counter are device
     pointers valid in this process (own, or mapped with mandel_ipc_open).
     want_stats=False: the render is only enqueued on ``stream``; returns None."""
@@ -349,7 +355,7 @@ def mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, dtype, scheme,
     o = _opts(chunk_rows=chunk_rows, tile_px=tile_px, kernel=kernel, refill_lanes=refill_lanes,
               ilp=ilp, min_ctas=min_ctas, adapt_lo=adapt_lo, adapt_hi=adapt_hi,
               check_every=check_every, tile_rows=tile_rows, no_pack=no_pack, band_out=band_out,
-              max_sms=max_sms, stage=stage, fused_y=fused_y)
+              max_sms=max_sms, stage=stage, fused_y=fused_y, first_block=first_block)
     rc = lib().mandel_render_rank(xmin, xmax, ymin, ymax, W, H, iter_max, R, _enum(dtype, DTYPES),
                                   _enum(scheme, SCHEMES), rank, nranks, ctypes.byref(o),
                                   root_p, _ptr(fcfs_counter), stream,

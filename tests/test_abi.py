@@ -50,7 +50,7 @@ def test_library_is_sm100a_only(mandel):
 
 
 def test_abi_version_and_strerror(mandel):
-    assert mandel.mandel_abi_version() == 9
+    assert mandel.mandel_abi_version() == 10
     for code in range(-7, 1):
         assert mandel.strerror(code) and mandel.strerror(code) != "unknown status"
 

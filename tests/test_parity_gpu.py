@@ -886,3 +886,68 @@ def test_host_handoff_large_pinned(mandel, oracle):
     rows = np.sort(np.random.default_rng(7).choice(cfg.H, 24, replace=False))
     want, _ = oracle.render_rows_mt(cfg, rows)
     _assert_same(m[rows], want, "C2 per-device hand-off rows")
+
+
+# ---------------------------------------------------------------------------
+# first block (options.first_block): a refill of many fresh pixels
+# starts with one exactly recorded block instead of a batch + replay -- counts unchanged
+# ---------------------------------------------------------------------------
+FIRST_BLOCK_VIEWS = {
+    "full": wl.C1.with_(W=328, H=203),                                   # exterior, boundary, interior
+    "far": wl.Config("far", 2.0, 9.0, -3.0, 3.0, 260, 130, 50, 2.0, "fp64"),  # every count 1 or 2
+    "seahorse": wl.Config("sea", -0.76, -0.73, 0.09, 0.12, 192, 160, 600, 2.0, "fp64"),
+}
+
+
+@pytest.mark.parametrize("view", sorted(FIRST_BLOCK_VIEWS))
+@pytest.mark.parametrize("kernel", ["refill", "batch8x1", "batch8x2", "batch8x3", "batch8x4", "batch4x2", "batch16x2"])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32", "fp64fma"])
+def test_first_block_parity(mandel, oracle, view, kernel, dtype):
+    if dtype == "fp32" and kernel.startswith("batch16"):
+        return  # fp32 allows check_every <= 8 (R18)
+    cfg = FIRST_BLOCK_VIEWS[view].with_(dtype=dtype)
+    want = oracle.render(cfg)
+    for fb in (0, -1, 1, 32):
+        out, st = _render_dev(mandel, cfg, "cyclic" if fb == 1 else "block", 1, kernel=kernel, first_block=fb)
+        _assert_same(_host(out), want, f"first_block={fb}/{view}/{kernel}/{dtype}")
+        if st["kernel"] == "eager" and st["kernel_batch"] > 1:
+            assert st["first_block"] == {0: 16, -1: 0, 1: 1, 32: 32}[fb]
+        else:
+            assert st["first_block"] == 0
+        assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
+
+
+@pytest.mark.parametrize("iter_max", [1, 2, 7, 8, 9, 15, 16, 17, 25])
+@pytest.mark.parametrize("dtype", ["fp64", "fp32"])
+def test_first_block_short_budgets(mandel, oracle, iter_max, dtype):
+    # budgets around the block length: below 8 the block is skipped, at 8 it is the whole
+    # budget (a slot that did not escape retires with iterMax), above it the batched loop follows
+    cfg = wl.C1.with_(W=200, H=120, iter_max=iter_max, dtype=dtype)
+    want = oracle.render(cfg)
+    for kernel in ("batch8x2", "batch8x1", "batch4x4"):
+        for fb in (1, 16):
+            out, st = _render_dev(mandel, cfg, "fcfs", 1, kernel=kernel, first_block=fb, chunk_rows=4)
+            _assert_same(_host(out), want, f"iterMax={iter_max}/{kernel}/first_block={fb}/{dtype}")
+
+
+def test_first_block_large_radius_and_bad_value(mandel, oracle):
+    # R = 2^100: slots past their escape inside the block overflow to inf/NaN; only the
+    # first escaping update is recorded
+    for dtype, R in (("fp64", 2.0 ** 100), ("fp32", 2.0 ** 20), ("fp64", 2.0 ** 200)):
+        cfg = wl.C1.with_(W=160, H=96, iter_max=40, R=R, dtype=dtype)
+        out, st = _render_dev(mandel, cfg, "block", 1, kernel="batch8x2", first_block=1)
+        _assert_same(_host(out), oracle.render(cfg), f"R={R}/{dtype}")
+    for bad in (-2, 33):
+        with pytest.raises(mandel.MandelError):
+            _render_dev(mandel, wl.C1.with_(W=64, H=64), "block", 1, first_block=bad)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_first_block_whole_map_matches_batched_form(mandel, name):
+    # the whole bench map with and without the first block, element by element
+    cfg = wl.CONFIGS[name]
+    a, sa = _render_dev(mandel, cfg, "block", 1, first_block=0)
+    b, sb = _render_dev(mandel, cfg, "block", 1, first_block=-1)
+    assert sa["first_block"] == 16 and sb["first_block"] == 0
+    assert bool((a == b).all()), f"{name}: the map with the first block differs from the batched form"
+    assert sa["sum_iters"] == sb["sum_iters"]

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--pack", default="1", help="fp32 packed batched loop: 1, 0 or 1,0")
     ap.add_argument("--stage", default="0", help="store staging: 1 staged, -1 direct, 0 default (comma list)")
     ap.add_argument("--fused-y", default="0", help="options.fused_y (0 on, -1 off)")
+    ap.add_argument("--first-block", default="0", help="options.first_block (0 default, -1 off, 1..32 lanes)")
     ap.add_argument("--ctas", default="0", help="resident CTAs per SM cap (0 = occupancy max), comma list")
     ap.add_argument("--chunks", default="16")
     ap.add_argument("--lanes", default="0", help="LAZY refill_lanes (0 = the library default, 16)")
@@ -65,7 +66,7 @@ def main():
                 continue
             kw = dict(out_dev0=out, stream0=stream.cuda_stream, kernel=kern,
                       tile_px=int(tile), tile_rows=int(trows), chunk_rows=int(chunk), refill_lanes=int(lanes),
-                      no_pack=pack == "0", stage=int(stage), ctas_per_sm=int(ctas), fused_y=int(a.fused_y),
+                      no_pack=pack == "0", stage=int(stage), ctas_per_sm=int(ctas), fused_y=int(a.fused_y), first_block=int(a.first_block),
                       min_ctas=int(minb) if kern != "static" else 0, adapt_lo=alo, adapt_hi=ahi)
             out.zero_()
             for _ in range(a.warmup):
