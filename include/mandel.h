@@ -226,7 +226,7 @@ typedef struct mandel_options {
                                 instead of a batch that would hit and be replayed -- the warp is
                                 in the exterior, where counts are a few updates.  Counts are
                                 identical either way.  0 -> default
-                                (16); -1 -> never; otherwise MANDEL_EINVAL                        */
+                                (2); -1 -> never; otherwise MANDEL_EINVAL                         */
 } mandel_options;
 
 /*

@@ -351,7 +351,7 @@ struct KernelChoice {
 constexpr KernelChoice kDefaultChoice[3] = {{MANDEL_KERNEL_EAGER, 2, 3, 8, 0, 0},    // fp64
                                             {MANDEL_KERNEL_EAGER, 1, 3, 8, 0, 4},    // fp32
                                             {MANDEL_KERNEL_EAGER, 2, 3, 8, 0, 0}};   // fp64 FMA
-constexpr uint32_t kDefaultFirstBlock = 16;   // options.first_block
+constexpr uint32_t kDefaultFirstBlock = 2;    // options.first_block (lanes)
 constexpr uint32_t kDefaultRefillLanes = 16;  // LAZY on C4: 8 -> 1509, 16 -> 1555 Giter/s
 constexpr uint32_t kDefaultAdaptLo = 8, kDefaultAdaptHi = 16;  // C2 1653, C4 1546, C5 1824 Giter/s
 constexpr double kDefaultBandTaper = 0.7;  // band pair p holds a 0.7^p share of the rows
@@ -631,7 +631,7 @@ int build_params(const Derived& d, uint32_t W, uint32_t H, uint32_t iter_max, in
     if (rl < 1 || rl > 32) return fail(MANDEL_EINVAL, "options.refill_lanes must be in 1..32");
     p.refill_lanes = (uint32_t)rl;
     // first block (mandel_kernels.cuh): lanes' worth of fresh slots
-    // that start one (C2: off 5.17, 8 -> 5.01, 16 -> 5.03, 32 -> 5.06 ms; profiles/r02ar_*)
+    // that start one (C2: off 5.17, 1 -> 5.00, 4 -> 5.01, 16 -> 5.03, 32 -> 5.06 ms; profiles/r02as_*, r02at_*)
     const int fb = o ? o->first_block : 0;
     if (fb < -1 || fb > 32) return fail(MANDEL_EINVAL, "options.first_block must be -1 or in 0..32");
     p.first_block = fb < 0 ? 0xffffffffu : (uint32_t)((fb ? fb : (int)kDefaultFirstBlock) * kc.ilp);

@@ -911,7 +911,7 @@ def test_first_block_parity(mandel, oracle, view, kernel, dtype):
         out, st = _render_dev(mandel, cfg, "cyclic" if fb == 1 else "block", 1, kernel=kernel, first_block=fb)
         _assert_same(_host(out), want, f"first_block={fb}/{view}/{kernel}/{dtype}")
         if st["kernel"] == "eager" and st["kernel_batch"] > 1:
-            assert st["first_block"] == {0: 16, -1: 0, 1: 1, 32: 32}[fb]
+            assert st["first_block"] == {0: 2, -1: 0, 1: 1, 32: 32}[fb]
         else:
             assert st["first_block"] == 0
         assert st["sum_iters"] == int(want.sum(dtype=np.uint64))
@@ -948,6 +948,6 @@ def test_first_block_whole_map_matches_batched_form(mandel, name):
     cfg = wl.CONFIGS[name]
     a, sa = _render_dev(mandel, cfg, "block", 1, first_block=0)
     b, sb = _render_dev(mandel, cfg, "block", 1, first_block=-1)
-    assert sa["first_block"] == 16 and sb["first_block"] == 0
+    assert sa["first_block"] == 2 and sb["first_block"] == 0
     assert bool((a == b).all()), f"{name}: the map with the first block differs from the batched form"
     assert sa["sum_iters"] == sb["sum_iters"]

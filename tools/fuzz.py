@@ -123,6 +123,8 @@ def main():
             kw = {}
             if mandel.KERNELS[kern][2:] and cfg.R < 2.0:
                 kw["check_every"] = 1
+            if mandel.KERNELS[kern][2:] or kern == "refill":  # first-block threshold (a scheduling decision only)
+                kw["first_block"] = int(rng.choice([0, 0, -1, 1, 2, 8, 31, 32]))
             if kern.startswith("lazy"):  # the LAZY exit threshold (a refill decision only)
                 kw["refill_lanes"] = int(rng.choice([1, 2, 7, 16, 31, 32]))
             for scheme, n in (("fcfs", 1), ("cyclic", 3)):
