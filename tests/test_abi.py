@@ -148,3 +148,36 @@ def test_binding_validates_output_buffers(mandel):
         with pytest.raises(mandel.MandelError) as e:
             mandel.mandel_render(*cfg.args(), "fp64", "block", 1, np.zeros((cfg.H, cfg.W), np.uint32))
         assert e.value.code == mandel.MANDEL_ENODEV
+
+
+def test_binding_structs_match_the_header(mandel, tmp_path):
+    """The ctypes mirrors of mandel_options / mandel_stats have the header's layout: a C
+    program compiled against include/mandel.h prints every field's offset and the struct
+    sizes (a field added to one side only would shift everything after it silently)."""
+    import ctypes
+    import os
+    import re
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hdr = open(os.path.join(root, "include", "mandel.h")).read()
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "mandel.h"', 'int main(void) {']
+    want = {}
+    for cname, ctype in (("mandel_options", mandel.mandel_options), ("mandel_stats", mandel.mandel_stats)):
+        end = re.search(r"\}\s*" + cname + r"\s*;", hdr).start()
+        body = hdr[hdr.rindex("{", 0, end) + 1:end]
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        fields = [re.sub(r"\[.*", "", f.strip().split()[-1]) for f in body.split(";") if f.strip()]
+        assert fields == [f[0] for f in ctype._fields_], f"{cname}: field names/order differ from the header"
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        want[cname] = ctypes.sizeof(ctype)
+        for f in fields:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+            want[f"{cname}.{f}"] = getattr(ctype, f).offset
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(root, "include"), "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    got = {k: int(v) for k, v in (l.split() for l in out.splitlines())}
+    assert got == want
