@@ -1,4 +1,6 @@
 set -x
+# NOTE: ran against the first prototype (threshold from the MANDEL_FIRST_BLOCK_MIN environment variable, since replaced by
+# options.first_block) and A/B builds libmandel_fb4/fb6.so = -DMANDEL_FIRST_BLOCK=4/6 (build.build_debug)
 # first-block A/B: MANDEL_FIRST_BLOCK_MIN (lanes' worth of fresh slots; 0 = off) x block length 8 / 6 / 4
 S=gpurun_out/r02ar_sweep_first_block.jsonl; : > $S
 run() { # lib fb configs

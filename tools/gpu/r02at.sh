@@ -1,4 +1,6 @@
 set -x
+# NOTE: libmandel_fbP.so = -DMANDEL_FIRST_BLOCK=P -DMANDEL_FB_ENV=1 A/B builds; MANDEL_FB_ENV (threshold in slots from the
+# MANDEL_FB_SLOTS environment variable) existed only for this sweep and is not in the library
 # first block: block length (4..16, -DMANDEL_FIRST_BLOCK) x threshold in slots (MANDEL_FB_SLOTS; A/B builds only)
 S=gpurun_out/r02at_sweep_first_block_len.jsonl; : > $S
 run() { # lib slots configs

@@ -1,4 +1,6 @@
 set -x
+# NOTE: libmandel_vA_B.so = A/B builds of a first block with early-exit votes after updates A and B (not adopted,
+# DESIGN.md "Tried: early-exit votes inside the first block"); the code is not in the tree
 # first block with early-exit votes (all of the warp's pixels escaped) after updates A and B: A/B builds
 S=gpurun_out/r02av_sweep_first_block_vote.jsonl; : > $S
 run() { # lib configs
